@@ -1,0 +1,159 @@
+"""Seeded synthetic inputs shared by the oracle, the tests and bench.py.
+
+This module holds NONE of the DG method's arithmetic (no basis, operators,
+geometry, flux or time stepping).  It only produces what a user would hand to
+``dg_setup`` / ``dg_set_fields`` / ``dg_run``:
+
+* the structured unit-square triangulation of SURVEY.md §8(c) A16
+  (vertex id = j*(nx+1)+i; cell (i,j) -> elements 2(j*nx+i) = (v00,v10,v11)
+  and 2(j*nx+i)+1 = (v00,v11,v01), both counter-clockwise);
+* the exact PEC-cavity mode of the (corrected) TM system
+  (eq. 2a-c with the A1 reading), formula as SPEC.md:431;
+* the exact two-layer cavity mode for the
+  piecewise-constant material extension (A12);
+* seeded perturbations (np.random.default_rng(20261017));
+* a CFL time-step estimate (dt is a caller input, A13).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+SEED = 20261017
+
+
+# ----------------------------------------------------------------------------
+# Mesh
+# ----------------------------------------------------------------------------
+def rect_mesh(nx: int, ny: int | None = None, x0=0.0, x1=1.0, y0=0.0, y1=1.0):
+    """Structured triangulation of [x0,x1]x[y0,y1] into 2*nx*ny CCW triangles.
+
+    Returns (VX, VY, EToV) with EToV int64 [K][3], 0-based.
+    """
+    if ny is None:
+        ny = nx
+    if nx < 1 or ny < 1 or not (x1 > x0 and y1 > y0):
+        raise ValueError("degenerate rectangle mesh request")
+    xs = np.linspace(x0, x1, nx + 1)
+    ys = np.linspace(y0, y1, ny + 1)
+    VX = np.tile(xs, ny + 1)
+    VY = np.repeat(ys, nx + 1)
+    i = np.tile(np.arange(nx), ny)
+    j = np.repeat(np.arange(ny), nx)
+    v00 = j * (nx + 1) + i
+    v10 = v00 + 1
+    v01 = v00 + (nx + 1)
+    v11 = v01 + 1
+    EToV = np.empty((2 * nx * ny, 3), dtype=np.int64)
+    EToV[0::2] = np.stack([v00, v10, v11], axis=1)
+    EToV[1::2] = np.stack([v00, v11, v01], axis=1)
+    return VX, VY, EToV
+
+
+def two_layer_material(VX, VY, EToV, eps_right=2.25, x_interface=0.5):
+    """Piecewise-constant eps (1 | eps_right at x = x_interface), mu = 1 (config C5)."""
+    xc = VX[EToV].mean(axis=1)
+    eps = np.where(xc > x_interface, eps_right, 1.0)
+    mu = np.ones_like(eps)
+    return eps, mu
+
+
+# ----------------------------------------------------------------------------
+# Exact solutions
+# ----------------------------------------------------------------------------
+def cavity_mode(x, y, t, m=1, n=1):
+    """Exact PEC unit-square cavity mode.
+
+    Ez = sin(m pi x) sin(n pi y) cos(w t)
+    Hx = -(n pi / w) sin(m pi x) cos(n pi y) sin(w t)
+    Hy =  (m pi / w) cos(m pi x) sin(n pi y) sin(w t),   w = pi sqrt(m^2+n^2)
+    """
+    w = math.pi * math.sqrt(m * m + n * n)
+    sx, cx = np.sin(m * math.pi * x), np.cos(m * math.pi * x)
+    sy, cy = np.sin(n * math.pi * y), np.cos(n * math.pi * y)
+    Ez = sx * sy * math.cos(w * t)
+    Hx = -(n * math.pi / w) * sx * cy * math.sin(w * t)
+    Hy = (m * math.pi / w) * cx * sy * math.sin(w * t)
+    return Hx, Hy, Ez
+
+
+def two_layer_omega(eps1=1.0, eps2=2.25, mu1=1.0, mu2=1.0):
+    """First root w (both k_i real) of (k1/mu1) cot(k1/2) = -(k2/mu2) cot(k2/2),
+    k_i^2 = w^2 eps_i mu_i - pi^2 (y-mode 1).
+    Written as k1/mu1 cos(k1/2) sin(k2/2) + k2/mu2 cos(k2/2) sin(k1/2) = 0."""
+    def f(w):
+        k1 = math.sqrt(w * w * eps1 * mu1 - math.pi ** 2)
+        k2 = math.sqrt(w * w * eps2 * mu2 - math.pi ** 2)
+        return (k1 / mu1) * math.cos(k1 / 2) * math.sin(k2 / 2) + \
+               (k2 / mu2) * math.cos(k2 / 2) * math.sin(k1 / 2)
+    # scan upward from where both wavenumbers are real for the first sign change, then bisect
+    w0 = math.pi / math.sqrt(min(eps1 * mu1, eps2 * mu2)) * (1 + 1e-9)
+    step = 1e-3
+    a = w0
+    fa = f(a)
+    while True:
+        b = a + step
+        fb = f(b)
+        if fa == 0.0:
+            return a
+        if fa * fb < 0:
+            break
+        a, fa = b, fb
+        if a > 100:
+            raise RuntimeError("no root found")
+    for _ in range(200):
+        mid = 0.5 * (a + b)
+        fm = f(mid)
+        if fa * fm <= 0:
+            b = mid
+        else:
+            a, fa = mid, fm
+    return 0.5 * (a + b)
+
+
+def two_layer_mode(x, y, t, side, eps1=1.0, eps2=2.25, mu1=1.0, mu2=1.0, omega=None):
+    """Exact two-layer cavity mode.
+
+    ``side`` is 0 (x < 1/2, eps1) or 1 (x > 1/2, eps2) per point; each element
+    takes X from its own side so the interface sits on element faces.
+    """
+    w = omega if omega is not None else two_layer_omega(eps1, eps2, mu1, mu2)
+    k1 = math.sqrt(w * w * eps1 * mu1 - math.pi ** 2)
+    k2 = math.sqrt(w * w * eps2 * mu2 - math.pi ** 2)
+    C = math.sin(k1 / 2) / math.sin(k2 / 2)
+    side = np.asarray(side)
+    X = np.where(side == 0, np.sin(k1 * x), C * np.sin(k2 * (1 - x)))
+    dX = np.where(side == 0, k1 * np.cos(k1 * x), -C * k2 * np.cos(k2 * (1 - x)))
+    mu = np.where(side == 0, mu1, mu2)
+    Ez = X * np.sin(math.pi * y) * math.cos(w * t)
+    Hx = -(math.pi / (mu * w)) * X * np.cos(math.pi * y) * math.sin(w * t)
+    Hy = (1.0 / (mu * w)) * dX * np.sin(math.pi * y) * math.sin(w * t)
+    return Hx, Hy, Ez
+
+
+def perturbation(shape, amplitude=1e-3, seed=SEED):
+    """Seeded normal perturbation [3][...] (Hx, Hy, Ez), SURVEY.md §8(d)."""
+    rng = np.random.default_rng(seed)
+    return amplitude * rng.standard_normal((3,) + tuple(shape))
+
+
+# ----------------------------------------------------------------------------
+# Time step (a caller input, A13)
+# ----------------------------------------------------------------------------
+def cfl_dt(VX, VY, EToV, N, cfl=1.0, eps=None, mu=None):
+    """dt = cfl * (2/3) * min_k(r_in,k * sqrt(eps_k mu_k)) * (x1 - x0) where
+    r_in is the inscribed radius and x0 < x1 the first two Gauss-Legendre nodes
+    of order N+1 (numpy.polynomial.legendre.leggauss)."""
+    P = np.stack([VX[EToV], VY[EToV]], axis=-1)
+    l0 = np.linalg.norm(P[:, 1] - P[:, 0], axis=1)
+    l1 = np.linalg.norm(P[:, 2] - P[:, 1], axis=1)
+    l2 = np.linalg.norm(P[:, 0] - P[:, 2], axis=1)
+    sper = 0.5 * (l0 + l1 + l2)
+    area = np.sqrt(sper * (sper - l0) * (sper - l1) * (sper - l2))
+    rin = area / sper
+    if eps is not None:
+        rin = rin * np.sqrt(np.asarray(eps) * (np.asarray(mu) if mu is not None else 1.0))
+    g = np.sort(np.polynomial.legendre.leggauss(N + 1)[0])
+    rmin = abs(g[1] - g[0]) if N >= 1 else 2.0
+    return cfl * (2.0 / 3.0) * float(rin.min()) * rmin
