@@ -1,0 +1,75 @@
+// Internal interface between the runtime (runtime.cu) and the per-(N, precision)
+// kernel modules (inst/k_N*_f*.cu, each its own CUDA module with its own
+// __constant__ bank holding Dr, Ds and LIFT).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dg {
+
+// Device data layout ("tile-blocked"): elements are grouped
+// in tiles of TILE = 32 (one warp lane per element).  A field f of the local
+// partition is stored as  f[t][n][lane]  (t = k / 32, lane = k % 32, n = node),
+// i.e. offset (t*Np + n)*32 + lane, followed by the halo "ghost" face values.
+// Every warp-wide access to node n of a tile is one contiguous 128 B (fp32) /
+// 256 B (fp64) transaction.
+constexpr int TILE = 32;
+
+// Per-tile geometry block: geo[t][c][lane], NGEO components.
+//   c = 0..3   rx, sx, ry, sy
+//   c = 4+3f   nx_f,  5+3f ny_f,  6+3f hF_f                 (f = 0,1,2)
+//              hF = Fsc/2 (constant material, the 1/2 of reading A3) or Fsc (material)
+//   c = 13+f   Bsc_f  (+1 interior, -1 PEC, reading A7)
+//   material only (NGEO_MAT):
+//   c = 16, 17 1/mu, 1/eps
+//   c = 18+4f  wEH = Y+/(Y+ + Y-), wHH = alpha/(Y+ + Y-), wHE = Z+/(Z+ + Z-), wEE = alpha/(Z+ + Z-)
+constexpr int NGEO_CONST = 16;
+constexpr int NGEO_MAT = 32;
+
+enum StageMode : int {
+  MODE_FUSED_RK = 0,    // volume + flux + LIFT + LSERK4 update (one kernel per stage)
+  MODE_VOLUME = 1,      // volume term only -> out (split mode, and dg_eval_rhs(1))
+  MODE_SURFACE_RK = 2,  // flux + LIFT added to rhsV (in), then the LSERK4 update
+  MODE_RHS = 3,         // full d/dt -> out (dg_eval_rhs(0))
+  MODE_SURFACE = 4,     // surface term only -> out (dg_eval_rhs(2))
+};
+
+struct StageArgs {
+  const void* q_in;        // [3][fstride] T, tile-blocked + ghosts
+  void* q_out;             // [3][fstride] T   (RK modes)
+  void* res;               // [3][vstride] T   (RK modes, read if a != 0, written if write_res)
+  const void* rhsv;        // [3][vstride] T   (MODE_SURFACE_RK)
+  void* out;               // [3][vstride] T   (MODE_VOLUME / MODE_RHS / MODE_SURFACE)
+  const void* geo;         // [ntiles][NGEO][32] T
+  const int32_t* vmapP;    // [ntiles][3 Nfp][32] offsets into a field (tile-blocked or ghost)
+  const int32_t* tiles;    // optional list of tile ids to process (NULL: 0..ntiles-1)
+  int64_t fstride;         // elements between fields of q (local + ghosts)
+  int64_t vstride;         // elements between fields of res / rhsv / out
+  int32_t ntiles;          // number of tiles to process (length of `tiles` if given)
+  int32_t write_res;       // RK modes: store the residual (0 on the last stage)
+  int32_t scale_volume;    // MODE_VOLUME with material: apply 1/mu, 1/eps (dg_eval_rhs only)
+  double a, b, dt;         // LSERK4 stage coefficients and step
+  double alpha;            // flux parameter (constant-material kernels)
+};
+
+struct KernelInfo {
+  int N, prec;                       // prec = 4 or 8
+  int threads, tiles_per_cta, row_groups, rows_per_group;
+  size_t smem_bytes;
+};
+
+struct KernelModule {
+  int N = 0, prec = 0;
+  // upload Dr, Ds [Np][Np], LIFT [Np][3Nfp] (fp64 host, rounded once to T) to this module's
+  // constant bank on the current device
+  cudaError_t (*upload)(const double* Dr, const double* Ds, const double* LIFT) = nullptr;
+  // launch one stage kernel; material selects the A12 flux
+  cudaError_t (*launch)(int mode, bool material, const StageArgs& a, cudaStream_t s) = nullptr;
+  KernelInfo (*info)() = nullptr;
+  bool (*check_fmask)(const int* Fmask) = nullptr;
+};
+
+// Registry: one entry per compiled (N, prec); nullptr if not compiled.
+const KernelModule* find_module(int N, int prec);
+
+}  // namespace dg
