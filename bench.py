@@ -1,0 +1,330 @@
+"""Benchmark: DG DOF-updates/s of the LSERK4 TM-Maxwell step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--order N] [--n CELLS] [--prec 4|8] [--split]
+
+Default workload = config C4 (BASELINE.json configs[3], the north-star target):
+unit-square PEC cavity, A16 mesh of 724 x 724 cells (K = 1,048,352 triangles),
+N = 5, fp32, cavity mode (1,1) initial data, dt from the CFL estimate.  One
+"step" = one LSERK4 step = 5 stage launches of the fused volume+flux+LIFT+RK
+kernel over every element.  metric value = Np * K * 3 fields * 5 stages * steps
+/ (max over ranks of the CUDA-event time of the K timed steps); inputs are
+resident in HBM when the timed region starts; the working set (~0.8 GB at
+C4) is larger than the 126 MB L2, so no explicit flush is needed.
+
+Under torchrun (N > 1) every rank owns a contiguous block of elements
+(SURVEY.md §8(e)); face traces cross ranks by NCCL send/recv inside the stage
+loop (strong scaling: K fixed).
+
+--impl reference times the fp64 NumPy oracle (oracle/, the only "reference"
+this paper-only task has) on host cores, on a bounded sample of the same
+workload per step; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import dginputs  # noqa: E402
+
+METRIC = "DG DOF-updates/s (fp32/fp64) and % of kernel roofline at 1/2/4/8 B200"
+UNIT = "DOF-updates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes_per_element_stage(Np, s):
+    """Bytes the method must move per element per LSERK4 stage, averaged over the 5 stages
+    (DESIGN.md §Roofline): q_in read + q_out write (6 Np) + residual read on stages 1-4 and
+    write on stages 0-3 (2 * 0.8 * 3 Np) in the arithmetic type (s bytes), + 13 geometry words
+    (rx, sx, ry, sy; nx, ny, Fsc per face) in the arithmetic type + 4 words of connectivity
+    (3 neighbour ids + packed face ids).  Neighbour traces are L2 hits (not DRAM)."""
+    return (6.0 + 4.8) * Np * s + 13 * s + 16
+
+
+def flops_per_element_stage(N):
+    Np, Nfp = (N + 1) * (N + 2) // 2, N + 1
+    vol = 8 * Np * Np + 8 * Np            # 4 mat-vecs (FMA = 2) + chain rule / curl
+    lift = 2 * 3 * Np * 3 * Nfp           # LIFT on 3 fields
+    flux = 3 * Nfp * 3 * 12               # jumps + upwind flux per face point
+    rk = 3 * Np * 4                       # res = a res + dt rhs; q += b res
+    return vol + lift + flux + rk
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[3:7]) if v.strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def workload(args):
+    N, n, prec = args.order, args.n, args.prec
+    VX, VY, E = dginputs.rect_mesh(n)
+    K = E.shape[0]
+    Np = (N + 1) * (N + 2) // 2
+    dt = dginputs.cfl_dt(VX, VY, E, N)
+    name = (f"C4-shaped: 2D TM Maxwell PEC unit-square cavity, N={N}, K={K:,} triangles "
+            f"({n}x{n} A16 mesh), {'fp32' if prec == 4 else 'fp64'}, LSERK4, cavity mode (1,1)")
+    return VX, VY, E, K, Np, dt, name
+
+
+def oracle_sample(N, n_sample, steps):
+    """Time the fp64 NumPy oracle (as it stands) on an n_sample x n_sample mesh."""
+    from oracle.solver import Oracle
+
+    VX, VY, E = dginputs.rect_mesh(n_sample)
+    o = Oracle(N, VX, VY, E)
+    q = dginputs.cavity_mode(o.geo.x, o.geo.y, 0.0)
+    dt = dginputs.cfl_dt(VX, VY, E, N)
+    t0 = time.perf_counter()
+    o.run(q, dt, steps)
+    sec = time.perf_counter() - t0
+    dof = o.Np * o.K * 3 * 5 * steps
+    return dof / sec, sec, o.K
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    N = args.order
+    _, _, _, K, Np, _, name = workload(args)
+    n_sample = args.ref_n
+    from oracle.solver import Oracle
+
+    VX, VY, E = dginputs.rect_mesh(n_sample)
+    o = Oracle(N, VX, VY, E)
+    q = dginputs.cavity_mode(o.geo.x, o.geo.y, 0.0)
+    dt = dginputs.cfl_dt(VX, VY, E, N)
+    for _ in range(args.warmup):
+        q = o.run(q, dt, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        q = o.run(q, dt, 1)
+    sec = time.perf_counter() - t0
+    value = o.Np * o.K * 3 * 5 * args.steps / sec
+    sample = (f"fp64 NumPy oracle, N={N}, {n_sample}x{n_sample} A16 mesh (K={o.K}) per step, "
+              f"{args.steps} steps after {args.warmup} warm-up")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": name, "reference_sample_K": o.K},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_1304_5546_b200 import dg
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist_
+
+        dist = dist_
+        ids = [dg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        nccl_id = ids[0]
+    VX, VY, E, K, Np, dt, name = workload(args)
+    ctx = dg.dg_setup(args.order, VX, VY, E, precision=args.prec, device=local_rank, rank=rank,
+                      nranks=world, fused=not args.split, transport=0, nccl_id=nccl_id)
+    x, y = ctx.nodes()
+    q0 = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in dginputs.cavity_mode(x, y, 0.0)]
+    ctx.set_fields(*q0)
+    stream = torch.cuda.ExternalStream(ctx.stream())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    ctx.run(dt, args.warmup)
+    ctx.sync()
+    # timed region: exactly K steps, kernel events on the library's stream
+    ctx.profile(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
+                      else local_rank) as clk:
+        time.sleep(0.3)
+        barrier()
+        t_wall = time.perf_counter()
+        e0.record(stream)
+        ctx.run(dt, args.steps)
+        e1.record(stream)
+        e1.synchronize()
+        t_wall = time.perf_counter() - t_wall
+        barrier()
+    ms = e0.elapsed_time(e1)
+    stats = ctx.kernel_stats()
+    ctx.profile(False)
+    ctx.sync()
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = Np * K * 3 * 5 * args.steps / (ms * 1e-3)
+    # dominant kernel roofline
+    kind = "volume" if args.split else "fused"
+    launches = sum(v["launches"] for v in stats.values())
+    s = args.prec
+    hbm, peak_src = peaks()
+    if args.split:
+        # split mode: report the surface+RK kernel (the larger share) separately in config
+        kind = max(("volume", "surface"), key=lambda k: stats[k]["ms"])
+    k_ms = stats[kind]["ms"] / max(stats[kind]["timed"], 1)
+    K_local = ctx.K_local
+    abytes = algorithmic_bytes_per_element_stage(Np, s) * K_local
+    achieved = abytes / (k_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(f"N{args.order}_p{s}_n{args.n}_P{world}_{kind}")
+            traffic = tr
+    except Exception:
+        pass
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": traffic, "kernel": f"stage_kernel<{kind}>", "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": abytes, "avg_launch_ms": k_ms,
+            "flops_per_launch": flops_per_element_stage(args.order) * K_local,
+            "achieved_tflops": flops_per_element_stage(args.order) * K_local / (k_ms * 1e-3) / 1e12}
+    # e2e through the public API with host buffers (job level: set fields, K steps, get fields)
+    barrier()
+    outs = [torch.empty_like(a).pin_memory() for a in q0]
+    t0 = time.perf_counter()
+    ctx.set_fields(*q0)
+    ctx.run(dt, args.steps)
+    ctx.get_fields(outs)
+    e2e_sec = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_sec], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_sec = float(t.item())
+    fbytes = 3 * K * Np * 8
+    e2e = {"value": Np * K * 3 * 5 * args.steps / e2e_sec, "unit": UNIT,
+           "h2d_bytes_per_step": fbytes / args.steps, "d2h_bytes_per_step": fbytes / args.steps,
+           "scope": "dg_set_fields(pinned host fp64) + dg_run(K steps) + dg_get_fields(pinned host fp64)"}
+    ctx.destroy()
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, sec, Ks = oracle_sample(args.order, args.ref_n, args.ref_steps)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"fp64 NumPy oracle (single-threaded), N={args.order}, K={Ks} "
+                         f"({args.ref_n}x{args.ref_n} mesh), {args.ref_steps} LSERK4 steps, {sec:.1f} s"}
+    ws_mb = (2 * 3 * (K // world) * Np * s + 3 * (K // world) * Np * s) / 1e6
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if s == 4 else "f64",
+            "data": "synthetic",
+            "config": {"workload": name, "N": args.order, "K": K, "Np": Np, "dt": dt,
+                       "variant": "split" if args.split else "fused", "parallelism": f"element-partition x{world}",
+                       "l2": f"no flush: per-GPU working set {ws_mb:.0f} MB > 126 MB L2"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "wall_s_timed": t_wall}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--order", type=int, default=5)
+    ap.add_argument("--n", type=int, default=724)
+    ap.add_argument("--prec", type=int, default=4, choices=[4, 8])
+    ap.add_argument("--split", action="store_true", help="volume + surface/RK kernels instead of fused")
+    ap.add_argument("--ref-n", type=int, default=48, help="oracle sample mesh cells per side")
+    ap.add_argument("--ref-steps", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -43,6 +43,7 @@ struct StageArgs {
   const void* geo;         // [ntiles][NGEO][32] T
   const int32_t* vmapP;    // [ntiles][3 Nfp][32] offsets into a field (tile-blocked or ghost)
   const int32_t* tiles;    // optional list of tile ids to process (NULL: 0..ntiles-1)
+  const void* ops;         // packed operators (KernelModule::pack_ops layout), device memory
   int64_t fstride;         // elements between fields of q (local + ghosts)
   int64_t vstride;         // elements between fields of res / rhsv / out
   int32_t ntiles;          // number of tiles to process (length of `tiles` if given)
@@ -54,15 +55,17 @@ struct StageArgs {
 
 struct KernelInfo {
   int N, prec;                       // prec = 4 or 8
-  int threads, tiles_per_cta, row_groups, rows_per_group;
+  int threads, slots, row_groups, rows_per_group;
   size_t smem_bytes;
 };
 
 struct KernelModule {
   int N = 0, prec = 0;
-  // upload Dr, Ds [Np][Np], LIFT [Np][3Nfp] (fp64 host, rounded once to T) to this module's
-  // constant bank on the current device
-  cudaError_t (*upload)(const double* Dr, const double* Ds, const double* LIFT) = nullptr;
+  // size of, and host packing into, the kernels' shared-memory operator layout:
+  // Dr, Ds [Np][Np], LIFT [Np][3Nfp] (fp64 host, rounded once to T); the runtime
+  // uploads the packed block once and passes it as StageArgs::ops
+  size_t (*ops_bytes)() = nullptr;
+  void (*pack_ops)(const double* Dr, const double* Ds, const double* LIFT, void* out) = nullptr;
   // launch one stage kernel; material selects the A12 flux
   cudaError_t (*launch)(int mode, bool material, const StageArgs& a, cudaStream_t s) = nullptr;
   KernelInfo (*info)() = nullptr;

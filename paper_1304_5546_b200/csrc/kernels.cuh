@@ -2,30 +2,34 @@
 //
 // Included once per translation unit (inst/k_N<N>_<prec>.cu) with
 //   DG_N   polynomial degree,  DG_T  float | double,  DG_TAG  e.g. N5_f32
-// so that every (N, T) is a separate CUDA module with its OWN __constant__
-// bank holding Dr, Ds (Np x Np) and LIFT (Np x 3Nfp).  Uniform (warp-wide
-// identical) operator entries are then fed to FFMA/DFMA straight from the
-// constant bank -- no shared-memory traffic for the operator at all.
+// so every (N, T) gets kernels with compile-time sizes (the paper's run-time
+// code generation, done as C++ templates).
 //
 // Work decomposition:
-//   * one warp lane per element, one warp per 32-element tile ("tile-blocked"
-//     layout, kernel_api.h) -- every field access of a warp is one contiguous
-//     128 B / 256 B line;
-//   * a tile's rows n are split over P "row-group" warps when the per-thread
-//     accumulators 3R (R rows) would exceed the register budget;
-//   * TPC tiles per CTA; the CTA first stages its tiles' Hx, Hy, Ez
-//     (cp.async 16 B, coalesced) and the neighbour traces q[vmapP]
-//     (cp.async 4/8 B gathers, mostly L2 hits) into shared memory, then each
-//     thread streams its element's column out of shared memory (conflict-free:
-//     lane = element).
+//   * one warp lane per element; a 32-element tile is owned by a "team" of
+//     P warps (one team per CTA), warp g computing output rows [gR, gR+R);
+//   * tile-blocked field layout (kernel_api.h): every warp access to node n of
+//     a tile is one contiguous 128 B / 256 B line, and a thread reading its
+//     element's column out of shared memory is bank-conflict free;
+//   * operators in shared memory ("matrix-in-local"), laid
+//     out so that one broadcast LDS.128 feeds 8 FFMA (fp32: Dr,Ds of two
+//     columns) or 4 DFMA (fp64); LIFT as (column pairs | columns) per row;
+//   * persistent CTAs walk their tiles with a cp.async software pipeline:
+//     while tile t is computed out of one shared-memory slot, tile t+1's
+//     Hx, Hy, Ez (16 B copies), geometry block and neighbour traces q[vmapP]
+//     (4/8 B gathers, mostly L2 hits; vmapP fetched one tile earlier) land in
+//     the other slot, and tile t's LSERK4 residual lands in its own buffer.
 //
-// Arithmetic per element (eq. 9, readings A1/A2; eq. 6 for the
-// chain rule; 1/2 eq. 5 flux, reading A3; A12 for materials):
-//   u = Dr Ez, v = Ds Ez                          -> rhsHx = -(ry u + sy v), rhsHy = rx u + sx v
-//   w = Dr (rx Hy - ry Hx) + Ds (sx Hy - sy Hx)   -> rhsEz = w   (= Dx Hy - Dy Hx, affine elements)
-//   rhs += LIFT (Fsc-scaled flux)
-//   res = a res + dt rhs;  q_out = q_in + b res   (LSERK4; A10)
+// Per tile, per stage (eq. 9 with readings A1/A2; eq. 6 chain
+// rule; 1/2 eq. 5 flux, reading A3; A12 for materials; LSERK4, A10):
+//   A  volume:  u = Dr Ez, v = Ds Ez;  w = Dr (rx Hy - ry Hx) + Ds (sx Hy - sy Hx)
+//               rhsHx = -(ry u + sy v), rhsHy = rx u + sx v, rhsEz = w
+//   B  flux:    per face point (split over the team), jumps [q] = q- - q+,
+//               Fsc-scaled upwind flux written in place of q+ in shared memory
+//   C  lift:    rhs += LIFT f
+//   D  update:  res = a res + dt rhs;  q_out = q_in + b res
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "kernel_api.h"
@@ -40,32 +44,46 @@
 namespace {
 
 using T = DG_T;
+constexpr bool F32 = sizeof(T) == 4;
 constexpr int N = DG_N;
 constexpr int NP = (N + 1) * (N + 2) / 2;
 constexpr int NFP = N + 1;
 constexpr int NF = 3 * NFP;
 constexpr int TL = dg::TILE;
 
-// register budget for the 3R row accumulators
-constexpr int RMAX = (sizeof(T) == 4) ? 28 : 16;
-constexpr int P = (NP + RMAX - 1) / RMAX;   // row-group warps per tile
-constexpr int R = (NP + P - 1) / P;         // rows per group
+// rows per warp and team size
+constexpr int R_TARGET = F32 ? 6 : 4;
+constexpr int P = (NP + R_TARGET - 1) / R_TARGET;  // warps per tile
+constexpr int R = (NP + P - 1) / P;                // rows per warp
+constexpr int RP = P * R;                          // padded rows (extra rows are zero)
+constexpr int TEAM = P * 32;
 
-constexpr size_t smem_per_tile(bool surf) {
-  return (size_t)(3 * NP + (surf ? 3 * NF : 0)) * TL * sizeof(T);
-}
-constexpr int choose_tpc() {
-  int t = 4 / P;
-  if (t < 1) t = 1;
-  while (t > 1 && smem_per_tile(true) * t > 96 * 1024) --t;
-  return t;
-}
-constexpr int TPC = choose_tpc();
-constexpr int THREADS = TPC * P * 32;
+// operator columns are consumed in groups of VC: fp32 pairs (one LDS.128 = Dr,Ds of 2 columns)
+constexpr int VC = F32 ? 2 : 1;
+constexpr int NPC = (NP + VC - 1) / VC;  // Dr/Ds column groups
+constexpr int NFC = (NF + VC - 1) / VC;  // LIFT column groups
+constexpr int NFE = NFC * VC;            // padded face points per element (flux buffer width)
 
-__constant__ T cDr[NP * NP];
-__constant__ T cDs[NP * NP];
-__constant__ T cLIFT[NP * NF];
+// shared-memory layout (bytes; each piece a multiple of 16 B)
+//   ops : DV[NPC][RP] (fp32 float4 {Dr_j, Ds_j, Dr_j+1, Ds_j+1} | fp64 double2 {Dr_j, Ds_j})
+//         LV[NFC][RP] (fp32 float2 {L_m, L_m+1} | fp64 double L_m)
+//   S slots of { q [3][NP][32], geo [NGEO][32], sp [3][NFE][32] }
+//   vm  [3][NF][32] int32 (vmapP of the next tiles),  res [3][NP][32]
+constexpr size_t DVB = (size_t)NPC * RP * 2 * VC * sizeof(T);
+constexpr size_t LVB = (size_t)NFC * RP * VC * sizeof(T);
+constexpr size_t OPB = ((DVB + LVB + 15) / 16) * 16;
+constexpr size_t QB = (size_t)3 * NP * TL * sizeof(T);
+__host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)(mat ? dg::NGEO_MAT : dg::NGEO_CONST) * TL * sizeof(T); }
+constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
+constexpr size_t VMB = (size_t)NF * TL * sizeof(int32_t);
+__host__ __device__ constexpr size_t slot_bytes(bool surf, bool mat) { return QB + geo_bytes(mat) + (surf ? SPB : 0); }
+__host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat, bool rk) {
+  return OPB + S * slot_bytes(surf, mat) + (surf ? 3 * VMB : 0) + (rk ? QB : 0);
+}
+// double-buffer when two teams still fit on an SM, else single-buffer
+__host__ __device__ constexpr int nslots(bool surf, bool mat, bool rk) { return smem_total(2, surf, mat, rk) <= 113 * 1024 ? 2 : 1; }
+constexpr int CTAS_BY_SMEM = (int)((227 * 1024) / smem_total(nslots(true, false, true), true, false, true));
+constexpr int MIN_CTAS = CTAS_BY_SMEM < 1 ? 1 : (CTAS_BY_SMEM > 8 ? 8 : CTAS_BY_SMEM);
 
 // Face node ids, increasing node index (closed form of the node ordering: row j
 // of the triangle starts at j(N+1) - j(j-1)/2).  Checked against the setup's
@@ -84,10 +102,10 @@ __device__ __forceinline__ void cp_async_small(void* s, const void* g) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(s));
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(sa), "l"(g), "n"(BYTES) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
 
 template <int MODE>
 struct ModeTraits {
@@ -96,216 +114,338 @@ struct ModeTraits {
   static constexpr bool rk = (MODE == dg::MODE_FUSED_RK || MODE == dg::MODE_SURFACE_RK);
 };
 
-// One row group G of one tile: rows [G R, G R + RR).
-template <int MODE, bool MAT, int G>
-__device__ __forceinline__ void tile_body(const dg::StageArgs& p, const T* __restrict__ sq,
-                                          const T* __restrict__ sp, int tile, int lane) {
-  using MT = ModeTraits<MODE>;
-  constexpr int NGEO = MAT ? dg::NGEO_MAT : dg::NGEO_CONST;
-  constexpr int n0 = G * R;
-  constexpr int RR = (NP - n0 < R) ? (NP - n0) : R;
-  const T* __restrict__ gg = static_cast<const T*>(p.geo) + (int64_t)tile * NGEO * TL + lane;
+using DV_t = typename std::conditional<F32, float4, double2>::type;
+using LV_t = typename std::conditional<F32, float2, double>::type;
 
-  T rhx[RR], rhy[RR], rez[RR];
-  if constexpr (MT::vol) {
-    const T rx = gg[0 * TL], sx = gg[1 * TL], ry = gg[2 * TL], sy = gg[3 * TL];
-    T u[RR], v[RR];
+// ---------------------------------------------------------------- phase A: volume
+template <typename DVT>  // DVT = DV_t (a template parameter so the other precision's branch is discarded)
+__device__ __forceinline__ void volume_rows(const T* __restrict__ sq, const DVT* __restrict__ DV, int n0, int lane,
+                                            T rx, T sx, T ry, T sy, T (&rhx)[R], T (&rhy)[R], T (&rez)[R]) {
+  T u[R], v[R];
 #pragma unroll
-    for (int r = 0; r < RR; ++r) { u[r] = T(0); v[r] = T(0); rez[r] = T(0); }
+  for (int r = 0; r < R; ++r) { u[r] = T(0); v[r] = T(0); rez[r] = T(0); }
+#pragma unroll 2
+  for (int jc = 0; jc < NPC; ++jc) {
+    if constexpr (F32) {
+      const int j0 = 2 * jc;
+      const int j1 = (2 * jc + 1 < NP) ? 2 * jc + 1 : NP - 1;  // pad column has zero Dr/Ds
+      const T hx0 = sq[(0 * NP + j0) * TL + lane], hx1 = sq[(0 * NP + j1) * TL + lane];
+      const T hy0 = sq[(1 * NP + j0) * TL + lane], hy1 = sq[(1 * NP + j1) * TL + lane];
+      const T ez0 = sq[(2 * NP + j0) * TL + lane], ez1 = sq[(2 * NP + j1) * TL + lane];
+      const T w10 = rx * hy0 - ry * hx0, w20 = sx * hy0 - sy * hx0;
+      const T w11 = rx * hy1 - ry * hx1, w21 = sx * hy1 - sy * hx1;
 #pragma unroll
-    for (int j = 0; j < NP; ++j) {
+      for (int r = 0; r < R; ++r) {
+        const DVT d = DV[jc * RP + n0 + r];
+        u[r] = fmaf(d.x, ez0, u[r]);
+        v[r] = fmaf(d.y, ez0, v[r]);
+        rez[r] = fmaf(d.x, w10, rez[r]);
+        rez[r] = fmaf(d.y, w20, rez[r]);
+        u[r] = fmaf(d.z, ez1, u[r]);
+        v[r] = fmaf(d.w, ez1, v[r]);
+        rez[r] = fmaf(d.z, w11, rez[r]);
+        rez[r] = fmaf(d.w, w21, rez[r]);
+      }
+    } else {
+      const int j = jc;
       const T hx = sq[(0 * NP + j) * TL + lane];
       const T hy = sq[(1 * NP + j) * TL + lane];
       const T ez = sq[(2 * NP + j) * TL + lane];
-      const T w1 = rx * hy - ry * hx;
-      const T w2 = sx * hy - sy * hx;
+      const T w1 = rx * hy - ry * hx, w2 = sx * hy - sy * hx;
 #pragma unroll
-      for (int r = 0; r < RR; ++r) {
-        const T dr = cDr[(n0 + r) * NP + j];
-        const T ds = cDs[(n0 + r) * NP + j];
-        u[r] = fma(dr, ez, u[r]);
-        v[r] = fma(ds, ez, v[r]);
-        rez[r] = fma(dr, w1, rez[r]);
-        rez[r] = fma(ds, w2, rez[r]);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < RR; ++r) {
-      rhx[r] = -(ry * u[r] + sy * v[r]);
-      rhy[r] = rx * u[r] + sx * v[r];
-    }
-  } else if constexpr (MODE == dg::MODE_SURFACE_RK) {
-    const T* __restrict__ rv = static_cast<const T*>(p.rhsv);
-#pragma unroll
-    for (int r = 0; r < RR; ++r) {
-      const int64_t off = ((int64_t)tile * NP + n0 + r) * TL + lane;
-      rhx[r] = rv[off];
-      rhy[r] = rv[p.vstride + off];
-      rez[r] = rv[2 * p.vstride + off];
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < RR; ++r) { rhx[r] = T(0); rhy[r] = T(0); rez[r] = T(0); }
-  }
-
-  if constexpr (MT::surf) {
-    const T alpha = static_cast<T>(p.alpha);
-#pragma unroll
-    for (int f = 0; f < 3; ++f) {
-      const T nx = gg[(4 + 3 * f) * TL], ny = gg[(5 + 3 * f) * TL], hF = gg[(6 + 3 * f) * TL];
-      const T bsc = gg[(13 + f) * TL];
-      T wEH = T(0), wHH = T(0), wHE = T(0), wEE = T(0);
-      if constexpr (MAT) {
-        wEH = gg[(18 + 4 * f) * TL];
-        wHH = gg[(19 + 4 * f) * TL];
-        wHE = gg[(20 + 4 * f) * TL];
-        wEE = gg[(21 + 4 * f) * TL];
-      }
-#pragma unroll
-      for (int i = 0; i < NFP; ++i) {
-        const int m = f * NFP + i;
-        const int fm = fmask(f, i);
-        const T hxm = sq[(0 * NP + fm) * TL + lane];
-        const T hym = sq[(1 * NP + fm) * TL + lane];
-        const T ezm = sq[(2 * NP + fm) * TL + lane];
-        const T hxp = sp[(0 * NF + m) * TL + lane];
-        const T hyp = sp[(1 * NF + m) * TL + lane];
-        const T ezp = sp[(2 * NF + m) * TL + lane];
-        const T dHx = hxm - hxp;
-        const T dHy = hym - hyp;
-        const T dEz = ezm - bsc * ezp;
-        T fHx, fHy, fEz;
-        if constexpr (!MAT) {
-          const T ndotdH = nx * dHx + ny * dHy;
-          fHx = hF * (ny * dEz + alpha * (nx * ndotdH - dHx));
-          fHy = hF * (-nx * dEz + alpha * (ny * ndotdH - dHy));
-          fEz = hF * (ny * dHx - nx * dHy - alpha * dEz);
-        } else {
-          const T dHt = nx * dHy - ny * dHx;
-          const T gH = wEH * dEz + wHH * dHt;
-          fHx = hF * (ny * gH);
-          fHy = -hF * (nx * gH);
-          fEz = -hF * (wHE * dHt + wEE * dEz);
-        }
-#pragma unroll
-        for (int r = 0; r < RR; ++r) {
-          const T L = cLIFT[(n0 + r) * NF + m];
-          rhx[r] = fma(L, fHx, rhx[r]);
-          rhy[r] = fma(L, fHy, rhy[r]);
-          rez[r] = fma(L, fEz, rez[r]);
-        }
+      for (int r = 0; r < R; ++r) {
+        const DVT d = DV[j * RP + n0 + r];
+        u[r] = fma(d.x, ez, u[r]);
+        v[r] = fma(d.y, ez, v[r]);
+        rez[r] = fma(d.x, w1, rez[r]);
+        rez[r] = fma(d.y, w2, rez[r]);
       }
     }
   }
-
-  // material factors 1/mu, 1/eps (reading A12).  In split mode the volume kernel
-  // writes the UNSCALED rhsV and the surface kernel scales the sum.
-  if constexpr (MAT) {
-    if (MODE != dg::MODE_VOLUME || p.scale_volume) {
-      const T imu = gg[16 * TL], ieps = gg[17 * TL];
 #pragma unroll
-      for (int r = 0; r < RR; ++r) { rhx[r] *= imu; rhy[r] *= imu; rez[r] *= ieps; }
-    }
+  for (int r = 0; r < R; ++r) {
+    rhx[r] = -(ry * u[r] + sy * v[r]);
+    rhy[r] = rx * u[r] + sx * v[r];
   }
+}
 
-  if constexpr (MT::rk) {
-    T* __restrict__ res = static_cast<T*>(p.res);
-    T* __restrict__ qo = static_cast<T*>(p.q_out);
-    const T a = static_cast<T>(p.a), b = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
-    const bool read_res = p.a != 0.0;
-#pragma unroll
-    for (int r = 0; r < RR; ++r) {
-      const int n = n0 + r;
-      const int64_t off = ((int64_t)tile * NP + n) * TL + lane;
-      const T rhs[3] = {rhx[r], rhy[r], rez[r]};
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        T rs = dt * rhs[c];
-        if (read_res) rs = fma(a, res[c * p.vstride + off], rs);
-        if (p.write_res) res[c * p.vstride + off] = rs;
-        qo[c * p.fstride + off] = fma(b, rs, sq[(c * NP + n) * TL + lane]);
-      }
+// ---------------------------------------------------------------- phase B: flux
+// Face points m = g, g+P, ... of this thread's element; the Fsc-scaled flux
+// (the vector f^k of eq. 8) overwrites the neighbour trace q+ in place.
+template <bool MAT>
+__device__ __forceinline__ void flux_points(const T* __restrict__ sq, const T* __restrict__ gg, T* __restrict__ sp,
+                                            int g, int lane, T alpha) {
+  for (int m = g; m < NF; m += P) {
+    const int f = m / NFP;
+    const int i = m - f * NFP;
+    const int fm = f == 0 ? i : (f == 1 ? row_start(i) + N - i : row_start(i));
+    const T nx = gg[(4 + 3 * f) * TL], ny = gg[(5 + 3 * f) * TL], hF = gg[(6 + 3 * f) * TL];
+    const T bsc = gg[(13 + f) * TL];
+    const T dHx = sq[(0 * NP + fm) * TL + lane] - sp[(0 * NFE + m) * TL + lane];
+    const T dHy = sq[(1 * NP + fm) * TL + lane] - sp[(1 * NFE + m) * TL + lane];
+    const T dEz = sq[(2 * NP + fm) * TL + lane] - bsc * sp[(2 * NFE + m) * TL + lane];
+    T fHx, fHy, fEz;
+    if constexpr (!MAT) {
+      const T ndotdH = nx * dHx + ny * dHy;
+      fHx = hF * (ny * dEz + alpha * (nx * ndotdH - dHx));
+      fHy = hF * (-nx * dEz + alpha * (ny * ndotdH - dHy));
+      fEz = hF * (ny * dHx - nx * dHy - alpha * dEz);
+    } else {
+      const T wEH = gg[(18 + 4 * f) * TL], wHH = gg[(19 + 4 * f) * TL];
+      const T wHE = gg[(20 + 4 * f) * TL], wEE = gg[(21 + 4 * f) * TL];
+      const T dHt = nx * dHy - ny * dHx;
+      const T gH = wEH * dEz + wHH * dHt;
+      fHx = hF * (ny * gH);
+      fHy = -hF * (nx * gH);
+      fEz = -hF * (wHE * dHt + wEE * dEz);
     }
-  } else {
-    T* __restrict__ out = static_cast<T*>(p.out);
+    sp[(0 * NFE + m) * TL + lane] = fHx;
+    sp[(1 * NFE + m) * TL + lane] = fHy;
+    sp[(2 * NFE + m) * TL + lane] = fEz;
+  }
+}
+
+// ---------------------------------------------------------------- phase C: lift
+template <typename LVT>
+__device__ __forceinline__ void lift_rows(const T* __restrict__ sp, const LVT* __restrict__ LV, int n0, int lane,
+                                          T (&rhx)[R], T (&rhy)[R], T (&rez)[R]) {
+#pragma unroll 3
+  for (int mc = 0; mc < NFC; ++mc) {
+    if constexpr (F32) {
+      const int m0 = 2 * mc, m1 = 2 * mc + 1;  // m1 may be the zero pad column
+      const T a0 = sp[(0 * NFE + m0) * TL + lane], a1 = sp[(0 * NFE + m1) * TL + lane];
+      const T b0 = sp[(1 * NFE + m0) * TL + lane], b1 = sp[(1 * NFE + m1) * TL + lane];
+      const T c0 = sp[(2 * NFE + m0) * TL + lane], c1 = sp[(2 * NFE + m1) * TL + lane];
 #pragma unroll
-    for (int r = 0; r < RR; ++r) {
-      const int64_t off = ((int64_t)tile * NP + n0 + r) * TL + lane;
-      out[off] = rhx[r];
-      out[p.vstride + off] = rhy[r];
-      out[2 * p.vstride + off] = rez[r];
+      for (int r = 0; r < R; ++r) {
+        const LVT l = LV[mc * RP + n0 + r];
+        rhx[r] = fmaf(l.x, a0, rhx[r]);
+        rhy[r] = fmaf(l.x, b0, rhy[r]);
+        rez[r] = fmaf(l.x, c0, rez[r]);
+        rhx[r] = fmaf(l.y, a1, rhx[r]);
+        rhy[r] = fmaf(l.y, b1, rhy[r]);
+        rez[r] = fmaf(l.y, c1, rez[r]);
+      }
+    } else {
+      const int m = mc;
+      const T a0 = sp[(0 * NFE + m) * TL + lane];
+      const T b0 = sp[(1 * NFE + m) * TL + lane];
+      const T c0 = sp[(2 * NFE + m) * TL + lane];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const LVT l = LV[m * RP + n0 + r];
+        rhx[r] = fma(l, a0, rhx[r]);
+        rhy[r] = fma(l, b0, rhy[r]);
+        rez[r] = fma(l, c0, rez[r]);
+      }
     }
   }
 }
 
-template <int MODE, bool MAT, int G>
-__device__ __forceinline__ void dispatch_group(int g, const dg::StageArgs& p, const T* sq, const T* sp,
-                                               int tile, int lane) {
-  if constexpr (G < P) {
-    if (g == G) tile_body<MODE, MAT, G>(p, sq, sp, tile, lane);
-    else dispatch_group<MODE, MAT, G + 1>(g, p, sq, sp, tile, lane);
-  }
-}
-
+// Persistent, software-pipelined stage kernel (one team per CTA).
 template <int MODE, bool MAT>
-__global__ void __launch_bounds__(THREADS) stage_kernel(const dg::StageArgs p) {
+__global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageArgs p) {
   using MT = ModeTraits<MODE>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sq = reinterpret_cast<T*>(smem_raw);          // [TPC][3][NP][32]
-  T* sp = sq + (size_t)TPC * 3 * NP * TL;          // [TPC][3][NF][32]
-  const T* __restrict__ q = static_cast<const T*>(p.q_in);
-  const int slot0 = blockIdx.x * TPC;
-
-  // ---- stage this CTA's tiles and their neighbour traces into shared memory
+  constexpr int NG = MAT ? dg::NGEO_MAT : dg::NGEO_CONST;
+  constexpr int S = nslots(MT::surf, MAT, MT::rk);
+  constexpr size_t SLOT = slot_bytes(MT::surf, MAT);
+  constexpr size_t GB = geo_bytes(MAT);
   constexpr int CH = 16 / (int)sizeof(T);
-  constexpr int CHUNKS = NP * TL / CH;  // 16 B chunks per field tile
-  for (int i = threadIdx.x; i < TPC * 3 * CHUNKS; i += THREADS) {
-    const int tl = i / (3 * CHUNKS);
-    const int rem = i - tl * 3 * CHUNKS;
-    const int c = rem / CHUNKS;
-    const int ch = rem - c * CHUNKS;
-    const int slot = slot0 + tl;
-    if (slot >= p.ntiles) continue;
-    const int tile = p.tiles ? p.tiles[slot] : slot;
-    cp_async16(sq + ((size_t)tl * 3 + c) * NP * TL + ch * CH, q + c * p.fstride + (int64_t)tile * NP * TL + ch * CH);
-  }
-  if constexpr (MT::surf) {
-    for (int i = threadIdx.x; i < TPC * NF * TL; i += THREADS) {
-      const int tl = i / (NF * TL);
-      const int rem = i - tl * NF * TL;  // m*32 + lane
-      const int slot = slot0 + tl;
-      if (slot >= p.ntiles) continue;
-      const int tile = p.tiles ? p.tiles[slot] : slot;
-      const int idx = __ldg(p.vmapP + (int64_t)tile * NF * TL + rem);
+  constexpr int QC = NP * TL / CH;  // 16 B chunks per field tile
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const T* __restrict__ q = static_cast<const T*>(p.q_in);
+  const T* __restrict__ geo = static_cast<const T*>(p.geo);
+  const int tid = threadIdx.x;
+  const int first = blockIdx.x, stride = gridDim.x;
+  const int n_it = first < p.ntiles ? (p.ntiles - first + stride - 1) / stride : 0;
+  if (n_it == 0) return;
+
+  const DV_t* DV = reinterpret_cast<const DV_t*>(smem_raw);
+  const LV_t* LV = reinterpret_cast<const LV_t*>(smem_raw + DVB);
+  unsigned char* slots = smem_raw + OPB;
+  auto sq_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT); };
+  auto sg_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB); };
+  auto sp_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB + GB); };
+  auto vm_of = [&](int v) { return reinterpret_cast<int32_t*>(slots + S * SLOT + v * VMB); };
+  T* const sr = reinterpret_cast<T*>(slots + S * SLOT + (MT::surf ? 3 * VMB : 0));
+  const bool read_res = MT::rk && p.a != 0.0;
+
+  auto tile_of = [&](int it) {
+    const int sidx = first + it * stride;
+    return p.tiles ? p.tiles[sidx] : sidx;
+  };
+  auto issue_vm = [&](int it) {
+    const int4* src = reinterpret_cast<const int4*>(p.vmapP + (int64_t)tile_of(it) * NF * TL);
+    int4* dst = reinterpret_cast<int4*>(vm_of(it % 3));
+    for (int i = tid; i < NF * TL / 4; i += TEAM) cp_async16(dst + i, src + i);
+  };
+  auto issue_data = [&](int it) {
+    const int tile = tile_of(it);
+    const int s = it % S;
+    T* sq = sq_of(s);
+    for (int i = tid; i < 3 * QC; i += TEAM) {
+      const int c = i / QC, ch = i - c * QC;
+      cp_async16(sq + c * NP * TL + ch * CH, q + c * p.fstride + (int64_t)tile * NP * TL + ch * CH);
+    }
+    T* sg = sg_of(s);
+    const T* gsrc = geo + (int64_t)tile * NG * TL;
+    for (int i = tid; i < NG * TL / CH; i += TEAM) cp_async16(sg + i * CH, gsrc + i * CH);
+    if constexpr (MT::surf) {
+      const int32_t* v = vm_of(it % 3);
+      T* sp = sp_of(s);
+      for (int i = tid; i < NF * TL; i += TEAM) {
+        const int idx = v[i];
+        const int m = i >> 5, ln = i & 31;
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        cp_async_small<sizeof(T)>(sp + ((size_t)tl * 3 + c) * NF * TL + rem, q + c * p.fstride + idx);
+        for (int c = 0; c < 3; ++c)
+          cp_async_small<sizeof(T)>(sp + (c * NFE + m) * TL + ln, q + c * p.fstride + idx);
+      }
+    }
+  };
+
+  // prologue: operators (once per persistent CTA), zero flux pad columns, first tiles
+  {
+    const int4* src = reinterpret_cast<const int4*>(p.ops);
+    int4* dst = reinterpret_cast<int4*>(smem_raw);
+    for (int i = tid; i < (int)(OPB / 16); i += TEAM) cp_async16(dst + i, src + i);
+    if constexpr (MT::surf && NFE > NF) {
+      constexpr int PADN = (NFE - NF) * TL;
+      for (int i = tid; i < S * 3 * PADN; i += TEAM) {
+        const int s = i / (3 * PADN), rem = i - s * 3 * PADN;
+        const int c = rem / PADN, rem2 = rem - c * PADN;
+        sp_of(s)[(c * NFE + NF) * TL + rem2] = T(0);
+      }
     }
   }
+  if constexpr (MT::surf) issue_vm(0);
+  cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
+  issue_data(0);
+  if (MT::surf && n_it > 1) issue_vm(1);
+  cp_async_commit();
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tl = warp / P, g = warp - (warp / P) * P;
-  const int slot = slot0 + tl;
-  if (slot >= p.ntiles) return;
-  const int tile = p.tiles ? p.tiles[slot] : slot;
-  dispatch_group<MODE, MAT, 0>(g, p, sq + (size_t)tl * 3 * NP * TL, sp + (size_t)tl * 3 * NF * TL, tile, lane);
+  const int g = tid >> 5, lane = tid & 31;
+  const int n0 = g * R;
+  const T alpha = static_cast<T>(p.alpha);
+  for (int it = 0; it < n_it; ++it) {
+    cp_async_wait_all();
+    __syncthreads();
+    const int tile = tile_of(it);
+    if (read_res) {  // this tile's residual: its own group, committed BEFORE the next tile's data
+      const T* __restrict__ res = static_cast<const T*>(p.res);
+      for (int i = tid; i < 3 * QC; i += TEAM) {
+        const int c = i / QC, ch = i - c * QC;
+        cp_async16(sr + c * NP * TL + ch * CH, res + c * p.vstride + (int64_t)tile * NP * TL + ch * CH);
+      }
+    }
+    cp_async_commit();
+    if (S == 2 && it + 1 < n_it) {
+      issue_data(it + 1);
+      if (MT::surf && it + 2 < n_it) issue_vm(it + 2);
+    }
+    cp_async_commit();
+
+    const int s = it % S;
+    const T* sq = sq_of(s);
+    const T* gg = sg_of(s) + lane;
+    T* sp = sp_of(s);
+    T rhx[R], rhy[R], rez[R];
+    if constexpr (MT::vol) {
+      volume_rows(sq, DV, n0, lane, gg[0 * TL], gg[1 * TL], gg[2 * TL], gg[3 * TL], rhx, rhy, rez);
+    } else if constexpr (MODE == dg::MODE_SURFACE_RK) {
+      const T* __restrict__ rv = static_cast<const T*>(p.rhsv);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int n = n0 + r < NP ? n0 + r : NP - 1;
+        const int64_t off = ((int64_t)tile * NP + n) * TL + lane;
+        rhx[r] = rv[off];
+        rhy[r] = rv[p.vstride + off];
+        rez[r] = rv[2 * p.vstride + off];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) { rhx[r] = T(0); rhy[r] = T(0); rez[r] = T(0); }
+    }
+    if constexpr (MT::surf) {
+      flux_points<MAT>(sq, gg, sp, g, lane, alpha);
+      __syncthreads();
+      lift_rows(sp, LV, n0, lane, rhx, rhy, rez);
+    }
+    // material factors 1/mu, 1/eps (reading A12).  In split mode the volume kernel
+    // writes the UNSCALED rhsV and the surface kernel scales the sum.
+    if constexpr (MAT) {
+      if (MODE != dg::MODE_VOLUME || p.scale_volume) {
+        const T imu = gg[16 * TL], ieps = gg[17 * TL];
+#pragma unroll
+        for (int r = 0; r < R; ++r) { rhx[r] *= imu; rhy[r] *= imu; rez[r] *= ieps; }
+      }
+    }
+    if constexpr (MT::rk) {
+      T* __restrict__ res = static_cast<T*>(p.res);
+      T* __restrict__ qo = static_cast<T*>(p.q_out);
+      const T a = static_cast<T>(p.a), b = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
+      if (read_res) {
+        cp_async_wait_group<1>();
+        __syncthreads();
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int n = n0 + r;
+        if (RP != NP && n >= NP) break;
+        const int64_t off = ((int64_t)tile * NP + n) * TL + lane;
+        const T rhs[3] = {rhx[r], rhy[r], rez[r]};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          T rs = dt * rhs[c];
+          if (read_res) rs = fma(a, sr[(c * NP + n) * TL + lane], rs);
+          if (p.write_res) __stcs(res + c * p.vstride + off, rs);
+          __stcs(qo + c * p.fstride + off, fma(b, rs, sq[(c * NP + n) * TL + lane]));
+        }
+      }
+    } else {
+      T* __restrict__ out = static_cast<T*>(p.out);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int n = n0 + r;
+        if (RP != NP && n >= NP) break;
+        const int64_t off = ((int64_t)tile * NP + n) * TL + lane;
+        out[off] = rhx[r];
+        out[p.vstride + off] = rhy[r];
+        out[2 * p.vstride + off] = rez[r];
+      }
+    }
+    if (S == 1 && it + 1 < n_it) {
+      __syncthreads();
+      issue_data(it + 1);
+      if (MT::surf && it + 2 < n_it) issue_vm(it + 2);
+      cp_async_commit();
+    }
+  }
 }
 
 template <int MODE, bool MAT>
 cudaError_t launch_one(const dg::StageArgs& a, cudaStream_t s) {
-  constexpr size_t smem = TPC * smem_per_tile(ModeTraits<MODE>::surf);
-  static bool configured = false;  // per process; attribute is per device-function (set once)
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(stage_kernel<MODE, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  using MT = ModeTraits<MODE>;
+  constexpr size_t smem = smem_total(nslots(MT::surf, MAT, MT::rk), MT::surf, MAT, MT::rk);
+  static int grid_cap[64] = {0};  // resident CTAs (whole GPU) per device ordinal
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 64) return cudaErrorInvalidDevice;
+  if (grid_cap[dev] == 0) {
+    e = cudaFuncSetAttribute(stage_kernel<MODE, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    int per_sm = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_kernel<MODE, MAT>, TEAM, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    grid_cap[dev] = (per_sm > 0 ? per_sm : 1) * sms;
   }
-  const int grid = (a.ntiles + TPC - 1) / TPC;
-  if (grid == 0) return cudaSuccess;
-  stage_kernel<MODE, MAT><<<grid, THREADS, smem, s>>>(a);
+  const int grid = a.ntiles < grid_cap[dev] ? a.ntiles : grid_cap[dev];
+  if (grid <= 0) return cudaSuccess;
+  stage_kernel<MODE, MAT><<<grid, TEAM, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -325,17 +465,31 @@ cudaError_t launch(int mode, bool mat, const dg::StageArgs& a, cudaStream_t s) {
   }
 }
 
-cudaError_t upload(const double* Dr, const double* Ds, const double* LIFT) {
-  T h[NP * (NP > NF ? NP : NF)];
-  for (int i = 0; i < NP * NP; ++i) h[i] = static_cast<T>(Dr[i]);
-  cudaError_t e = cudaMemcpyToSymbol(cDr, h, sizeof(T) * NP * NP);
-  if (e != cudaSuccess) return e;
-  for (int i = 0; i < NP * NP; ++i) h[i] = static_cast<T>(Ds[i]);
-  e = cudaMemcpyToSymbol(cDs, h, sizeof(T) * NP * NP);
-  if (e != cudaSuccess) return e;
-  for (int i = 0; i < NP * NF; ++i) h[i] = static_cast<T>(LIFT[i]);
-  e = cudaMemcpyToSymbol(cLIFT, h, sizeof(T) * NP * NF);
-  return e;
+// Host: pack Dr, Ds [Np][Np] and LIFT [Np][3Nfp] (fp64, row-major) into the
+// kernels' shared-memory operator layout (rounded once to T; padded rows and
+// columns are zero).
+size_t ops_bytes() { return OPB; }
+void pack_ops(const double* Dr, const double* Ds, const double* LIFT, void* out) {
+  unsigned char* o = static_cast<unsigned char*>(out);
+  for (size_t i = 0; i < OPB; ++i) o[i] = 0;
+  T* dv = reinterpret_cast<T*>(o);
+  for (int jc = 0; jc < NPC; ++jc)
+    for (int n = 0; n < RP; ++n)
+      for (int k = 0; k < VC; ++k) {
+        const int j = jc * VC + k;
+        T* e = dv + ((size_t)(jc * RP + n) * VC + k) * 2;
+        if (n < NP && j < NP) {
+          e[0] = static_cast<T>(Dr[n * NP + j]);
+          e[1] = static_cast<T>(Ds[n * NP + j]);
+        }
+      }
+  T* lv = reinterpret_cast<T*>(o + DVB);
+  for (int mc = 0; mc < NFC; ++mc)
+    for (int n = 0; n < RP; ++n)
+      for (int k = 0; k < VC; ++k) {
+        const int m = mc * VC + k;
+        if (n < NP && m < NF) lv[(size_t)(mc * RP + n) * VC + k] = static_cast<T>(LIFT[n * NF + m]);
+      }
 }
 
 // the closed-form face masks compiled into the kernels must match the setup's node set
@@ -350,11 +504,11 @@ dg::KernelInfo info() {
   dg::KernelInfo k;
   k.N = N;
   k.prec = (int)sizeof(T);
-  k.threads = THREADS;
-  k.tiles_per_cta = TPC;
+  k.threads = TEAM;
+  k.slots = nslots(true, false, true);
   k.row_groups = P;
   k.rows_per_group = R;
-  k.smem_bytes = TPC * smem_per_tile(true);
+  k.smem_bytes = smem_total(nslots(true, false, true), true, false, true);
   return k;
 }
 
@@ -365,7 +519,8 @@ KernelModule DG_CAT(dg_module_, DG_TAG)() {
   KernelModule m;
   m.N = N;
   m.prec = (int)sizeof(T);
-  m.upload = &upload;
+  m.ops_bytes = &ops_bytes;
+  m.pack_ops = &pack_ops;
   m.launch = &launch;
   m.info = &info;
   m.check_fmask = &check_fmask;

@@ -175,6 +175,7 @@ struct dg_ctx {
   void* rhsv = nullptr;
   void* out = nullptr;
   void* geo = nullptr;
+  void* ops = nullptr;
   int32_t* vmapP = nullptr;
   int32_t* send_idx = nullptr;
   void* sendbuf = nullptr;
@@ -254,6 +255,7 @@ dg::StageArgs base_args(dg_ctx* c) {
   a.rhsv = c->rhsv;
   a.out = c->out;
   a.geo = c->geo;
+  a.ops = c->ops;
   a.vmapP = c->vmapP;
   a.tiles = nullptr;
   a.fstride = c->fstride;
@@ -428,7 +430,13 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
                                     " precision=" + std::to_string(c->prec));
   if (!c->km->check_fmask(c->ref.Fmask.data()))
     return set_err(DG_E_STATE, "kernel face masks disagree with the setup's node set");
-  CU(c, c->km->upload(c->ref.Dr.data(), c->ref.Ds.data(), c->ref.LIFT.data()));
+  {
+    std::vector<unsigned char> ops(c->km->ops_bytes());
+    c->km->pack_ops(c->ref.Dr.data(), c->ref.Ds.data(), c->ref.LIFT.data(), ops.data());
+    dg_status st0 = alloc(c, &c->ops, ops.size());
+    if (st0 != DG_OK) return st0;
+    CU(c, cudaMemcpy(c->ops, ops.data(), ops.size(), cudaMemcpyHostToDevice));
+  }
   const int Np = c->ref.Np;
   c->tsz = (size_t)c->prec;
   c->ngeo = c->material ? dg::NGEO_MAT : dg::NGEO_CONST;
@@ -925,7 +933,7 @@ void dg_destroy(dg_ctx* c) {
       Nccl* n = nccl();
       if (n) (c->poisoned ? n->CommAbort : n->CommDestroy)(c->nccl_comm);
     }
-    void* bufs[] = {c->q[0], c->q[1], c->res, c->rhsv, c->out, c->geo, c->vmapP, c->send_idx,
+    void* bufs[] = {c->q[0], c->q[1], c->res, c->rhsv, c->out, c->geo, c->ops, c->vmapP, c->send_idx,
                     c->sendbuf, c->stage, c->flag, c->tiles_int, c->tiles_bnd};
     for (void* b : bufs)
       if (b) cudaFree(b);
