@@ -52,7 +52,7 @@ constexpr int NF = 3 * NFP;
 constexpr int TL = dg::TILE;
 
 // rows per warp and team size
-constexpr int R_TARGET = F32 ? 6 : 4;
+constexpr int R_TARGET = F32 ? 8 : 6;              // max rows per warp
 constexpr int P = (NP + R_TARGET - 1) / R_TARGET;  // warps per tile
 constexpr int R = (NP + P - 1) / P;                // rows per warp
 constexpr int RP = P * R;                          // padded rows (extra rows are zero)
@@ -77,8 +77,9 @@ __host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)(mat ?
 constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
 constexpr size_t VMB = (size_t)NF * TL * sizeof(int32_t);
 __host__ __device__ constexpr size_t slot_bytes(bool surf, bool mat) { return QB + geo_bytes(mat) + (surf ? SPB : 0); }
+constexpr size_t BARB = 64;  // mbarriers: one per slot + one for the residual buffer
 __host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat, bool rk) {
-  return OPB + S * slot_bytes(surf, mat) + (surf ? 3 * VMB : 0) + (rk ? QB : 0);
+  return BARB + OPB + S * slot_bytes(surf, mat) + (surf ? 3 * VMB : 0) + (rk ? QB : 0);
 }
 // double-buffer when two teams still fit on an SM, else single-buffer
 __host__ __device__ constexpr int nslots(bool surf, bool mat, bool rk) { return smem_total(2, surf, mat, rk) <= 113 * 1024 ? 2 : 1; }
@@ -106,6 +107,32 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 template <int NPEND>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
+
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
 template <int MODE>
 struct ModeTraits {
@@ -176,7 +203,7 @@ template <bool MAT>
 __device__ __forceinline__ void flux_points(const T* __restrict__ sq, const T* __restrict__ gg, T* __restrict__ sp,
                                             int g, int lane, T alpha) {
   for (int m = g; m < NF; m += P) {
-    const int f = m / NFP;
+    const int f = m < NFP ? 0 : (m < 2 * NFP ? 1 : 2);
     const int i = m - f * NFP;
     const int fm = f == 0 ? i : (f == 1 ? row_start(i) + N - i : row_start(i));
     const T nx = gg[(4 + 3 * f) * TL], ny = gg[(5 + 3 * f) * TL], hF = gg[(6 + 3 * f) * TL];
@@ -260,9 +287,10 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   const int n_it = first < p.ntiles ? (p.ntiles - first + stride - 1) / stride : 0;
   if (n_it == 0) return;
 
-  const DV_t* DV = reinterpret_cast<const DV_t*>(smem_raw);
-  const LV_t* LV = reinterpret_cast<const LV_t*>(smem_raw + DVB);
-  unsigned char* slots = smem_raw + OPB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [0, S): slots, [S]: residual
+  const DV_t* DV = reinterpret_cast<const DV_t*>(smem_raw + BARB);
+  const LV_t* LV = reinterpret_cast<const LV_t*>(smem_raw + BARB + DVB);
+  unsigned char* slots = smem_raw + BARB + OPB;
   auto sq_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT); };
   auto sg_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB); };
   auto sp_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB + GB); };
@@ -279,34 +307,41 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     int4* dst = reinterpret_cast<int4*>(vm_of(it % 3));
     for (int i = tid; i < NF * TL / 4; i += TEAM) cp_async16(dst + i, src + i);
   };
-  auto issue_data = [&](int it) {
-    const int tile = tile_of(it);
-    const int s = it % S;
-    T* sq = sq_of(s);
-    for (int i = tid; i < 3 * QC; i += TEAM) {
-      const int c = i / QC, ch = i - c * QC;
-      cp_async16(sq + c * NP * TL + ch * CH, q + c * p.fstride + (int64_t)tile * NP * TL + ch * CH);
-    }
-    T* sg = sg_of(s);
-    const T* gsrc = geo + (int64_t)tile * NG * TL;
-    for (int i = tid; i < NG * TL / CH; i += TEAM) cp_async16(sg + i * CH, gsrc + i * CH);
-    if constexpr (MT::surf) {
-      const int32_t* v = vm_of(it % 3);
-      T* sp = sp_of(s);
-      for (int i = tid; i < NF * TL; i += TEAM) {
-        const int idx = v[i];
-        const int m = i >> 5, ln = i & 31;
+  // fields + geometry of tile `it`: four TMA bulk copies issued by one thread
+  auto issue_tma = [&](int it) {
+    if (tid == 0) {
+      const int tile = tile_of(it);
+      const int s = it % S;
+      uint64_t* bar = bars + s;
+      mbar_expect_tx(bar, (unsigned)(QB + GB));
+      T* sq = sq_of(s);
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          cp_async_small<sizeof(T)>(sp + (c * NFE + m) * TL + ln, q + c * p.fstride + idx);
+      for (int c = 0; c < 3; ++c)
+        tma_load_1d(sq + c * NP * TL, q + c * p.fstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bar);
+      tma_load_1d(sg_of(s), geo + (int64_t)tile * NG * TL, (unsigned)GB, bar);
+    }
+  };
+  // neighbour traces of tile `it` (needs its vmapP in vm[it % 3])
+  auto issue_gather = [&](int it) {
+    if constexpr (MT::surf) {
+      const int32_t* v = vm_of(it % 3) + (tid & 31);
+      T* sp = sp_of(it % S) + (tid & 31);
+      for (int m = tid >> 5; m < NF; m += P) {
+        const T* src = q + v[m * TL];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cp_async_small<sizeof(T)>(sp + (c * NFE + m) * TL, src + c * p.fstride);
       }
     }
   };
 
-  // prologue: operators (once per persistent CTA), zero flux pad columns, first tiles
+  // prologue: barriers, operators (once per persistent CTA), zero flux pad columns, first tiles
+  if (tid == 0) {
+    for (int b = 0; b <= S; ++b) mbar_init(bars + b, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   {
     const int4* src = reinterpret_cast<const int4*>(p.ops);
-    int4* dst = reinterpret_cast<int4*>(smem_raw);
+    int4* dst = reinterpret_cast<int4*>(smem_raw + BARB);
     for (int i = tid; i < (int)(OPB / 16); i += TEAM) cp_async16(dst + i, src + i);
     if constexpr (MT::surf && NFE > NF) {
       constexpr int PADN = (NFE - NF) * TL;
@@ -321,7 +356,8 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  issue_data(0);
+  issue_tma(0);
+  issue_gather(0);
   if (MT::surf && n_it > 1) issue_vm(1);
   cp_async_commit();
 
@@ -329,24 +365,25 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   const int n0 = g * R;
   const T alpha = static_cast<T>(p.alpha);
   for (int it = 0; it < n_it; ++it) {
-    cp_async_wait_all();
+    const int s = it % S;
+    cp_async_wait_all();                     // gathers of tile it, vmapP of tile it+1
+    mbar_wait(bars + s, (unsigned)((it / S) & 1));  // TMA: fields + geometry of tile it
     __syncthreads();
     const int tile = tile_of(it);
-    if (read_res) {  // this tile's residual: its own group, committed BEFORE the next tile's data
+    if (read_res && tid == 0) {  // this tile's residual, consumed in the epilogue
+      mbar_expect_tx(bars + S, (unsigned)QB);
       const T* __restrict__ res = static_cast<const T*>(p.res);
-      for (int i = tid; i < 3 * QC; i += TEAM) {
-        const int c = i / QC, ch = i - c * QC;
-        cp_async16(sr + c * NP * TL + ch * CH, res + c * p.vstride + (int64_t)tile * NP * TL + ch * CH);
-      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        tma_load_1d(sr + c * NP * TL, res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bars + S);
     }
-    cp_async_commit();
     if (S == 2 && it + 1 < n_it) {
-      issue_data(it + 1);
+      issue_tma(it + 1);
+      issue_gather(it + 1);
       if (MT::surf && it + 2 < n_it) issue_vm(it + 2);
+      cp_async_commit();
     }
-    cp_async_commit();
 
-    const int s = it % S;
     const T* sq = sq_of(s);
     const T* gg = sg_of(s) + lane;
     T* sp = sp_of(s);
@@ -385,10 +422,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       T* __restrict__ res = static_cast<T*>(p.res);
       T* __restrict__ qo = static_cast<T*>(p.q_out);
       const T a = static_cast<T>(p.a), b = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
-      if (read_res) {
-        cp_async_wait_group<1>();
-        __syncthreads();
-      }
+      if (read_res) mbar_wait(bars + S, (unsigned)(it & 1));
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int n = n0 + r;
@@ -417,7 +451,8 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     }
     if (S == 1 && it + 1 < n_it) {
       __syncthreads();
-      issue_data(it + 1);
+      issue_tma(it + 1);
+      issue_gather(it + 1);
       if (MT::surf && it + 2 < n_it) issue_vm(it + 2);
       cp_async_commit();
     }
