@@ -94,10 +94,12 @@ Nccl* nccl() {
 }
 
 // ---------------------------------------------------------------- helper kernels
-// canonical fp64 [3][Kl][Np]  <->  tile-blocked T [3][fstride]
+// canonical fp64 [3][Kl][Np]  <->  tile-blocked T [3][fstride].  Device slot d
+// (tile d/32, lane d%32) holds local element perm[d] (-1: padding);
+// slot_of[kl] is the inverse.
 template <typename T>
-__global__ void to_blocked(const double* __restrict__ src, T* __restrict__ q, int64_t Kl, int64_t Kpad, int Np,
-                           int64_t fstride) {
+__global__ void to_blocked(const double* __restrict__ src, T* __restrict__ q, const int32_t* __restrict__ perm,
+                           int64_t Kl, int64_t Kpad, int Np, int64_t fstride) {
   const int64_t total = Kpad * Np;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i / total);
@@ -106,20 +108,22 @@ __global__ void to_blocked(const double* __restrict__ src, T* __restrict__ q, in
     const int64_t tn = o >> 5;
     const int64_t t = tn / Np;
     const int n = (int)(tn - t * Np);
-    const int64_t k = t * 32 + lane;
-    q[c * fstride + o] = (k < Kl) ? static_cast<T>(src[(c * Kl + k) * Np + n]) : T(0);
+    const int64_t kl = perm[t * 32 + lane];
+    q[c * fstride + o] = (kl >= 0) ? static_cast<T>(src[(c * Kl + kl) * Np + n]) : T(0);
   }
 }
 
 template <typename T>
-__global__ void from_blocked(const T* __restrict__ q, double* __restrict__ dst, int64_t Kl, int Np, int64_t fstride) {
+__global__ void from_blocked(const T* __restrict__ q, double* __restrict__ dst, const int32_t* __restrict__ slot_of,
+                             int64_t Kl, int Np, int64_t fstride) {
   const int64_t total = Kl * Np;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i / total);
-    const int64_t o = i - c * total;  // canonical k*Np + n
-    const int64_t k = o / Np;
-    const int n = (int)(o - k * Np);
-    dst[c * total + o] = static_cast<double>(q[c * fstride + ((k >> 5) * Np + n) * 32 + (k & 31)]);
+    const int64_t o = i - c * total;  // canonical kl*Np + n
+    const int64_t kl = o / Np;
+    const int n = (int)(o - kl * Np);
+    const int64_t d = slot_of[kl];
+    dst[c * total + o] = static_cast<double>(q[c * fstride + ((d >> 5) * Np + n) * 32 + (d & 31)]);
   }
 }
 
@@ -178,6 +182,9 @@ struct dg_ctx {
   void* ops = nullptr;
   int32_t* vmapP = nullptr;
   int32_t* send_idx = nullptr;
+  int32_t* perm_d = nullptr;     // [Kpad] device slot -> local element (-1 = padding)
+  int32_t* slot_of_d = nullptr;  // [Kl]   local element -> device slot
+  std::vector<int64_t> perm, slot_of;  // host copies
   void* sendbuf = nullptr;
   double* stage = nullptr;   // fp64 staging [3][Kl][Np]
   unsigned long long* flag = nullptr;
@@ -357,15 +364,23 @@ void upload_geometry(dg_ctx* c, std::vector<T>& g, std::vector<int32_t>& vp, con
   const dg::Mesh& m = c->mesh;
   g.assign((size_t)c->ntiles * ng * 32, T(0));
   vp.assign((size_t)c->ntiles * NF * 32, 0);
-  auto blk = [&](int64_t kl, int n) -> int64_t { return ((kl >> 5) * Np + n) * 32 + (kl & 31); };
-  for (int64_t kl = 0; kl < c->Kpad; ++kl) {
-    const int64_t t = kl >> 5, lane = kl & 31;
+  // blocked offset of node n of the element in device slot d
+  auto blk = [&](int64_t d, int n) -> int64_t { return ((d >> 5) * Np + n) * 32 + (d & 31); };
+  // neighbour node n of the element in slot d2, seen from slot d: same tile -> shared-memory
+  // offset within the tile's field block, encoded negative: -(1 + n*32 + lane2)
+  auto nbr_code = [&](int64_t d, int64_t d2, int n) -> int64_t {
+    if ((d >> 5) == (d2 >> 5)) return -(1 + (int64_t)n * 32 + (d2 & 31));
+    return blk(d2, n);
+  };
+  for (int64_t d = 0; d < c->Kpad; ++d) {
+    const int64_t t = d >> 5, lane = d & 31;
     auto G = [&](int comp) -> T& { return g[(t * ng + comp) * 32 + lane]; };
-    if (kl >= c->Kl) {
+    if (d >= c->Kl) {
       for (int f = 0; f < 3; ++f) G(13 + f) = T(1);
-      for (int mm = 0; mm < NF; ++mm) vp[(t * NF + mm) * 32 + lane] = (int32_t)blk(kl, 0);
+      for (int mm = 0; mm < NF; ++mm) vp[(t * NF + mm) * 32 + lane] = (int32_t)nbr_code(d, d, 0);
       continue;
     }
+    const int64_t kl = c->perm[d];
     G(0) = (T)m.rx[kl];
     G(1) = (T)m.sx[kl];
     G(2) = (T)m.ry[kl];
@@ -397,7 +412,7 @@ void upload_geometry(dg_ctx* c, std::vector<T>& g, std::vector<int32_t>& vp, con
       int64_t idx;
       if (nl >= 0) {
         const int64_t kl2 = nl / Np;
-        idx = blk(kl2, (int)(nl - kl2 * Np));
+        idx = nbr_code(d, c->slot_of[kl2], (int)(nl - kl2 * Np));
       } else {
         idx = c->ghost_base + (-nl - 1);
       }
@@ -450,6 +465,19 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
   c->vstride = c->Kpad * Np;
   if (c->fstride >= (int64_t)1 << 31) return set_err(DG_E_ARG, "partition too large for 32-bit face maps");
   dg_status st;
+  // device storage order: Morton order of the element centroids (setup.cpp locality_order)
+  c->perm = dg::locality_order(c->mesh);
+  c->slot_of.assign(c->Kl, 0);
+  for (int64_t d = 0; d < c->Kl; ++d) c->slot_of[c->perm[d]] = d;
+  {
+    std::vector<int32_t> pd(c->Kpad, -1), sd(std::max<int64_t>(c->Kl, 1), 0);
+    for (int64_t d = 0; d < c->Kl; ++d) pd[d] = (int32_t)c->perm[d];
+    for (int64_t kl = 0; kl < c->Kl; ++kl) sd[kl] = (int32_t)c->slot_of[kl];
+    if ((st = alloc(c, (void**)&c->perm_d, pd.size() * sizeof(int32_t))) != DG_OK) return st;
+    if ((st = alloc(c, (void**)&c->slot_of_d, sd.size() * sizeof(int32_t))) != DG_OK) return st;
+    CU(c, cudaMemcpy(c->perm_d, pd.data(), pd.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CU(c, cudaMemcpy(c->slot_of_d, sd.data(), sd.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
   for (int b = 0; b < 2; ++b)
     if ((st = alloc(c, &c->q[b], 3 * c->fstride * c->tsz)) != DG_OK) return st;
   if ((st = alloc(c, &c->res, 3 * c->vstride * c->tsz)) != DG_OK) return st;
@@ -482,8 +510,8 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
     for (int64_t s = 0; s < c->n_send; ++s) {
       const int64_t gd = c->mesh.send_gdof[s];
       const int64_t k = gd / Np, n = gd - (gd / Np) * Np;
-      const int64_t kl = c->mesh.g2l[k];
-      si[s] = (int32_t)(((kl >> 5) * Np + n) * 32 + (kl & 31));
+      const int64_t d = c->slot_of[c->mesh.g2l[k]];
+      si[s] = (int32_t)(((d >> 5) * Np + n) * 32 + (d & 31));
     }
     if ((st = alloc(c, (void**)&c->send_idx, si.size() * sizeof(int32_t))) != DG_OK) return st;
     CU(c, cudaMemcpy(c->send_idx, si.data(), si.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -491,7 +519,7 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
   }
   {
     std::vector<char> bnd(c->ntiles, 0);
-    for (int64_t p = 0; p < c->n_recv; ++p) bnd[(c->mesh.recv_point[p] / (3 * c->ref.Nfp)) >> 5] = 1;
+    for (int64_t p = 0; p < c->n_recv; ++p) bnd[c->slot_of[c->mesh.recv_point[p] / (3 * c->ref.Nfp)] >> 5] = 1;
     std::vector<int32_t> ti, tb;
     for (int64_t t = 0; t < c->ntiles; ++t) (bnd[t] ? tb : ti).push_back((int32_t)t);
     c->n_int = (int32_t)ti.size();
@@ -631,10 +659,10 @@ dg_status dg_set_fields(dg_ctx* c, const double* Hx, const double* Hy, const dou
     CU(c, cudaMemcpyAsync(c->stage + f * n, src[f], n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   void* q = c->q[c->cur];
   if (c->tsz == 4)
-    to_blocked<float><<<grid_for(3 * c->Kpad * c->ref.Np), 256, 0, c->stream>>>(c->stage, (float*)q, c->Kl, c->Kpad,
+    to_blocked<float><<<grid_for(3 * c->Kpad * c->ref.Np), 256, 0, c->stream>>>(c->stage, (float*)q, c->perm_d, c->Kl, c->Kpad,
                                                                                c->ref.Np, c->fstride);
   else
-    to_blocked<double><<<grid_for(3 * c->Kpad * c->ref.Np), 256, 0, c->stream>>>(c->stage, (double*)q, c->Kl,
+    to_blocked<double><<<grid_for(3 * c->Kpad * c->ref.Np), 256, 0, c->stream>>>(c->stage, (double*)q, c->perm_d, c->Kl,
                                                                                  c->Kpad, c->ref.Np, c->fstride);
   CU(c, cudaGetLastError());
   CU(c, cudaMemsetAsync(c->res, 0, 3 * c->vstride * c->tsz, c->stream));
@@ -650,9 +678,9 @@ dg_status dg_get_fields(dg_ctx* c, double* Hx, double* Hy, double* Ez) {
   const int64_t n = c->Kl * c->ref.Np;
   const void* q = c->q[c->cur];
   if (c->tsz == 4)
-    from_blocked<float><<<grid_for(3 * n), 256, 0, c->stream>>>((const float*)q, c->stage, c->Kl, c->ref.Np, c->fstride);
+    from_blocked<float><<<grid_for(3 * n), 256, 0, c->stream>>>((const float*)q, c->stage, c->slot_of_d, c->Kl, c->ref.Np, c->fstride);
   else
-    from_blocked<double><<<grid_for(3 * n), 256, 0, c->stream>>>((const double*)q, c->stage, c->Kl, c->ref.Np,
+    from_blocked<double><<<grid_for(3 * n), 256, 0, c->stream>>>((const double*)q, c->stage, c->slot_of_d, c->Kl, c->ref.Np,
                                                                  c->fstride);
   CU(c, cudaGetLastError());
   double* dst[3] = {Hx, Hy, Ez};
@@ -776,10 +804,10 @@ dg_status dg_eval_rhs(dg_ctx* c, int32_t which, double* rHx, double* rHy, double
   if ((st = launch_stage(c, mode, a, c->stream, which == 1 ? 1 : 2)) != DG_OK) return st;
   const int64_t n = c->Kl * c->ref.Np;
   if (c->tsz == 4)
-    from_blocked<float><<<grid_for(3 * n), 256, 0, c->stream>>>((const float*)c->out, c->stage, c->Kl, c->ref.Np,
+    from_blocked<float><<<grid_for(3 * n), 256, 0, c->stream>>>((const float*)c->out, c->stage, c->slot_of_d, c->Kl, c->ref.Np,
                                                                c->vstride);
   else
-    from_blocked<double><<<grid_for(3 * n), 256, 0, c->stream>>>((const double*)c->out, c->stage, c->Kl, c->ref.Np,
+    from_blocked<double><<<grid_for(3 * n), 256, 0, c->stream>>>((const double*)c->out, c->stage, c->slot_of_d, c->Kl, c->ref.Np,
                                                                 c->vstride);
   CU(c, cudaGetLastError());
   double* dst[3] = {rHx, rHy, rEz};
@@ -934,7 +962,7 @@ void dg_destroy(dg_ctx* c) {
       if (n) (c->poisoned ? n->CommAbort : n->CommDestroy)(c->nccl_comm);
     }
     void* bufs[] = {c->q[0], c->q[1], c->res, c->rhsv, c->out, c->geo, c->ops, c->vmapP, c->send_idx,
-                    c->sendbuf, c->stage, c->flag, c->tiles_int, c->tiles_bnd};
+                    c->sendbuf, c->stage, c->flag, c->tiles_int, c->tiles_bnd, c->perm_d, c->slot_of_d};
     for (void* b : bufs)
       if (b) cudaFree(b);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

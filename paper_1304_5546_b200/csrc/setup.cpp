@@ -596,4 +596,37 @@ void build_mesh(const RefElem& ref, int64_t Nv, const double* VX, const double* 
   }
 }
 
+std::vector<int64_t> locality_order(const Mesh& m) {
+  const int64_t Kl = (int64_t)m.local.size();
+  std::vector<double> cx(Kl), cy(Kl);
+  double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
+  for (int64_t kl = 0; kl < Kl; ++kl) {
+    const int64_t* v = &m.EToV[3 * m.local[kl]];
+    cx[kl] = (m.VX[v[0]] + m.VX[v[1]] + m.VX[v[2]]) / 3.0;
+    cy[kl] = (m.VY[v[0]] + m.VY[v[1]] + m.VY[v[2]]) / 3.0;
+    x0 = std::min(x0, cx[kl]); x1 = std::max(x1, cx[kl]);
+    y0 = std::min(y0, cy[kl]); y1 = std::max(y1, cy[kl]);
+  }
+  const double span = std::max(std::max(x1 - x0, y1 - y0), 1e-300);
+  auto spread = [](uint64_t v) {  // interleave the low 21 bits with zeros
+    v &= 0x1fffff;
+    v = (v | (v << 32)) & 0x1f00000000ffffULL;
+    v = (v | (v << 16)) & 0x1f0000ff0000ffULL;
+    v = (v | (v << 8)) & 0x100f00f00f00f00fULL;
+    v = (v | (v << 4)) & 0x10c30c30c30c30c3ULL;
+    v = (v | (v << 2)) & 0x1249249249249249ULL;
+    return v;
+  };
+  std::vector<std::pair<uint64_t, int64_t>> key(Kl);
+  for (int64_t kl = 0; kl < Kl; ++kl) {
+    const uint64_t ix = (uint64_t)std::min(2097151.0, std::floor((cx[kl] - x0) / span * 2097151.0));
+    const uint64_t iy = (uint64_t)std::min(2097151.0, std::floor((cy[kl] - y0) / span * 2097151.0));
+    key[kl] = {spread(ix) | (spread(iy) << 1), kl};
+  }
+  std::sort(key.begin(), key.end());
+  std::vector<int64_t> perm(Kl);
+  for (int64_t i = 0; i < Kl; ++i) perm[i] = key[i].second;
+  return perm;
+}
+
 }  // namespace dg

@@ -59,6 +59,12 @@ void build_mesh(const RefElem& ref, int64_t Nv, const double* VX, const double* 
                 const int64_t* EToV, const int8_t* bctag, int rank, int nranks, const int32_t* part,
                 Mesh& m);
 
+// Device storage order of the local elements: a permutation slot -> local id
+// sorted by the Morton (Z-order) code of the element centroids, so that a
+// 32-element tile is a compact patch and most face neighbours share its tile
+// (the "blocking strategy" against fetching faces twice).
+std::vector<int64_t> locality_order(const Mesh& m);
+
 // Canonical global maps for a local element (vmapM / vmapP of SURVEY.md §8(c) O7).
 void face_maps(const RefElem& ref, const Mesh& m, int64_t kl, int64_t* vmapM, int64_t* vmapP);
 
