@@ -51,15 +51,14 @@ constexpr int NFP = N + 1;
 constexpr int NF = 3 * NFP;
 constexpr int TL = dg::TILE;
 
-// Kernel family.  USE_W (fp32, Np <= 21): one warp owns a whole tile (all Np
-// rows), neighbour traces and residuals are prefetched into registers, the
-// flux is lifted straight from registers -- minimum instructions per FMA.
-// Otherwise a team of P warps shares each tile through shared memory.
-constexpr bool USE_W = false;  // (F32 && NP <= 21): register-resident variant, spills at Np = 21
-constexpr int WPC = 4;  // USE_W: independent warps (tiles in flight) per CTA
-
-// rows per warp and team size
-constexpr int R_TARGET = USE_W ? NP : (F32 ? 8 : 6);  // max rows per warp
+// rows per warp and team size (a team of P warps shares each tile)
+#ifndef DG_RMAX32
+#define DG_RMAX32 8
+#endif
+#ifndef DG_RMAX64
+#define DG_RMAX64 6
+#endif
+constexpr int R_TARGET = F32 ? DG_RMAX32 : DG_RMAX64;  // max rows per warp
 constexpr int P = (NP + R_TARGET - 1) / R_TARGET;     // warps per tile
 constexpr int R = (NP + P - 1) / P;                // rows per warp
 constexpr int RP = P * R;                          // padded rows (extra rows are zero)
@@ -77,7 +76,8 @@ constexpr int NFE = NFC * VC;            // padded face points per element (flux
 //   S slots of { q [3][NP][32], geo [NGEO][32], sp [3][NFE][32] }
 //   vm  [3][NF][32] int32 (vmapP of the next tiles),  res [3][NP][32]
 constexpr size_t DVB = (size_t)NPC * RP * 2 * VC * sizeof(T);
-constexpr size_t LVB = (size_t)NFC * RP * VC * sizeof(T);
+constexpr int RPL = (RP + 1) & ~1;  // LIFT rows padded to even
+constexpr size_t LVB = (size_t)NFC * RPL * VC * sizeof(T);
 constexpr size_t OPB = ((DVB + LVB + 15) / 16) * 16;
 constexpr size_t QB = (size_t)3 * NP * TL * sizeof(T);
 __host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)(mat ? dg::NGEO_MAT : dg::NGEO_CONST) * TL * sizeof(T); }
@@ -90,9 +90,6 @@ __host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat, bool
 }
 // double-buffer when two teams still fit on an SM, else single-buffer
 __host__ __device__ constexpr int nslots(bool surf, bool mat, bool rk) { return smem_total(2, surf, mat, rk) <= 113 * 1024 ? 2 : 1; }
-// USE_W layout: [2*WPC mbarriers][ops][WPC warps x 2 slots x {q, geo}]
-__host__ __device__ constexpr size_t w_slot_bytes(bool mat) { return QB + geo_bytes(mat); }
-__host__ __device__ constexpr size_t w_smem_total(bool mat) { return BARB + OPB + (size_t)WPC * 2 * w_slot_bytes(mat); }
 constexpr int CTAS_BY_SMEM = (int)((227 * 1024) / smem_total(nslots(true, false, true), true, false, true));
 constexpr int MIN_CTAS = CTAS_BY_SMEM < 1 ? 1 : (CTAS_BY_SMEM > 8 ? 8 : CTAS_BY_SMEM);
 
@@ -261,7 +258,7 @@ __device__ __forceinline__ void lift_rows(const T* __restrict__ sp, const LVT* _
       const T c0 = sp[(2 * NFE + m0) * TL + lane], c1 = sp[(2 * NFE + m1) * TL + lane];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const LVT l = LV[mc * RP + n0 + r];
+        const LVT l = LV[mc * RPL + n0 + r];
         rhx[r] = fmaf(l.x, a0, rhx[r]);
         rhy[r] = fmaf(l.x, b0, rhy[r]);
         rez[r] = fmaf(l.x, c0, rez[r]);
@@ -276,7 +273,7 @@ __device__ __forceinline__ void lift_rows(const T* __restrict__ sp, const LVT* _
       const T c0 = sp[(2 * NFE + m) * TL + lane];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const LVT l = LV[m * RP + n0 + r];
+        const LVT l = LV[m * RPL + n0 + r];
         rhx[r] = fma(l, a0, rhx[r]);
         rhy[r] = fma(l, b0, rhy[r]);
         rez[r] = fma(l, c0, rez[r]);
@@ -477,233 +474,8 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   }
 }
 
-__device__ __forceinline__ float lv_pick(float2 v, int k) { return k ? v.y : v.x; }
-__device__ __forceinline__ double lv_pick(double v, int) { return v; }
-
-// ---------------------------------------------------------------- USE_W kernel
-// Each warp walks its own tiles (warp gw handles tiles gw, gw + G, ...).  Per
-// tile: the fields + geometry arrive by TMA into one of the warp's two slots
-// (issued one tile ahead by lane 0); the neighbour traces q[vmapP] are
-// gathered straight into registers (vmapP itself read one tile ahead), the
-// residual is prefetched into registers after the volume phase, and each face
-// point's flux is lifted from registers.  No block-level synchronisation after
-// the prologue.
-template <int MODE, bool MAT>
-__global__ void __launch_bounds__(WPC * 32, 2) stage_kernel_w(const dg::StageArgs p) {
-  using MT = ModeTraits<MODE>;
-  constexpr int NG = MAT ? dg::NGEO_MAT : dg::NGEO_CONST;
-  constexpr size_t GB = geo_bytes(MAT);
-  constexpr size_t WS = w_slot_bytes(MAT);
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [WPC][2]
-  const DV_t* DV = reinterpret_cast<const DV_t*>(smem_raw + BARB);
-  const LV_t* LV = reinterpret_cast<const LV_t*>(smem_raw + BARB + DVB);
-  const T* __restrict__ q = static_cast<const T*>(p.q_in);
-  const T* __restrict__ geo = static_cast<const T*>(p.geo);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wsl = smem_raw + BARB + OPB + (size_t)w * 2 * WS;
-  uint64_t* wbar = bars + 2 * w;
-
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < 2 * WPC; ++b) mbar_init(bars + b, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  {
-    const int4* src = reinterpret_cast<const int4*>(p.ops);
-    int4* dst = reinterpret_cast<int4*>(smem_raw + BARB);
-    for (int i = threadIdx.x; i < (int)(OPB / 16); i += WPC * 32) cp_async16(dst + i, src + i);
-    cp_async_commit();
-    cp_async_wait_all();
-  }
-  __syncthreads();
-
-  const int gw = blockIdx.x * WPC + w, G = gridDim.x * WPC;
-  const int n_it = gw < p.ntiles ? (p.ntiles - gw + G - 1) / G : 0;
-  if (n_it == 0) return;
-  auto tile_of = [&](int it) {
-    const int sidx = gw + it * G;
-    return p.tiles ? p.tiles[sidx] : sidx;
-  };
-  auto issue_tma = [&](int it) {
-    if (lane == 0) {
-      const int tile = tile_of(it);
-      unsigned char* sl = wsl + (it & 1) * WS;
-      uint64_t* bar = wbar + (it & 1);
-      mbar_expect_tx(bar, (unsigned)WS);
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-        tma_load_1d(sl + c * (QB / 3), q + c * p.fstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bar);
-      tma_load_1d(sl + QB, geo + (int64_t)tile * NG * TL, (unsigned)GB, bar);
-    }
-  };
-  int32_t vmn[MT::surf ? NF : 1];
-  auto load_vm = [&](int it) {
-    if constexpr (MT::surf) {
-      const int32_t* v = p.vmapP + (int64_t)tile_of(it) * NF * TL + lane;
-#pragma unroll
-      for (int m = 0; m < NF; ++m) vmn[m] = __ldg(v + m * TL);
-    }
-  };
-  issue_tma(0);
-  load_vm(0);
-  const bool read_res = MT::rk && p.a != 0.0;
-  const T alpha = static_cast<T>(p.alpha);
-
-  for (int it = 0; it < n_it; ++it) {
-    const int tile = tile_of(it);
-    // neighbour traces of this tile -> registers (in flight during the volume phase)
-    T qp[3][MT::surf ? NF : 1];
-    int32_t vmc[MT::surf ? NF : 1];  // this tile's neighbour codes (negative: same tile)
-    if constexpr (MT::surf) {
-#pragma unroll
-      for (int m = 0; m < NF; ++m) {
-        vmc[m] = vmn[m];
-        if (vmc[m] >= 0) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) qp[c][m] = __ldg(q + c * p.fstride + vmc[m]);
-        }
-      }
-    }
-    if (it + 1 < n_it) load_vm(it + 1);
-    mbar_wait(wbar + (it & 1), (unsigned)((it >> 1) & 1));
-    __syncwarp();
-    if (it + 1 < n_it) issue_tma(it + 1);
-    const T* sq = reinterpret_cast<const T*>(wsl + (it & 1) * WS);
-    const T* gg = reinterpret_cast<const T*>(wsl + (it & 1) * WS + QB) + lane;
-
-    T rhx[R], rhy[R], rez[R];
-    if constexpr (MT::vol) {
-      volume_rows(sq, DV, 0, lane, gg[0 * TL], gg[1 * TL], gg[2 * TL], gg[3 * TL], rhx, rhy, rez);
-    } else if constexpr (MODE == dg::MODE_SURFACE_RK) {
-      const T* __restrict__ rv = static_cast<const T*>(p.rhsv);
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int64_t off = ((int64_t)tile * NP + r) * TL + lane;
-        rhx[r] = rv[off];
-        rhy[r] = rv[p.vstride + off];
-        rez[r] = rv[2 * p.vstride + off];
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < R; ++r) { rhx[r] = T(0); rhy[r] = T(0); rez[r] = T(0); }
-    }
-    // residual prefetch (in flight during the surface phase)
-    T rr[3][MT::rk ? NP : 1];
-    if constexpr (MT::rk) {
-      if (read_res) {
-        const T* __restrict__ res = static_cast<const T*>(p.res);
-#pragma unroll
-        for (int n = 0; n < NP; ++n)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) rr[c][n] = __ldcs(res + c * p.vstride + ((int64_t)tile * NP + n) * TL + lane);
-      }
-    }
-    if constexpr (MT::surf) {
-#pragma unroll
-      for (int m = 0; m < NF; ++m) {
-        const int f = m / NFP, i = m % NFP;
-        const int fm = fmask(f, i);
-        const T nx = gg[(4 + 3 * f) * TL], ny = gg[(5 + 3 * f) * TL], hF = gg[(6 + 3 * f) * TL];
-        const T bsc = gg[(13 + f) * TL];
-        T hxp = qp[0][m], hyp = qp[1][m], ezp = qp[2][m];
-        if (vmc[m] < 0) {  // same-tile neighbour
-          const T* pp = sq + (-1 - vmc[m]);
-          hxp = pp[0];
-          hyp = pp[NP * TL];
-          ezp = pp[2 * NP * TL];
-        }
-        const T dHx = sq[(0 * NP + fm) * TL + lane] - hxp;
-        const T dHy = sq[(1 * NP + fm) * TL + lane] - hyp;
-        const T dEz = sq[(2 * NP + fm) * TL + lane] - bsc * ezp;
-        T fHx, fHy, fEz;
-        if constexpr (!MAT) {
-          const T ndotdH = nx * dHx + ny * dHy;
-          fHx = hF * (ny * dEz + alpha * (nx * ndotdH - dHx));
-          fHy = hF * (-nx * dEz + alpha * (ny * ndotdH - dHy));
-          fEz = hF * (ny * dHx - nx * dHy - alpha * dEz);
-        } else {
-          const T wEH = gg[(18 + 4 * f) * TL], wHH = gg[(19 + 4 * f) * TL];
-          const T wHE = gg[(20 + 4 * f) * TL], wEE = gg[(21 + 4 * f) * TL];
-          const T dHt = nx * dHy - ny * dHx;
-          const T gH = wEH * dEz + wHH * dHt;
-          fHx = hF * (ny * gH);
-          fHy = -hF * (nx * gH);
-          fEz = -hF * (wHE * dHt + wEE * dEz);
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const T l = lv_pick(LV[(m / VC) * RP + r], m % VC);
-          rhx[r] = fmaf(l, fHx, rhx[r]);
-          rhy[r] = fmaf(l, fHy, rhy[r]);
-          rez[r] = fmaf(l, fEz, rez[r]);
-        }
-      }
-    }
-    if constexpr (MAT) {
-      if (MODE != dg::MODE_VOLUME || p.scale_volume) {
-        const T imu = gg[16 * TL], ieps = gg[17 * TL];
-#pragma unroll
-        for (int r = 0; r < R; ++r) { rhx[r] *= imu; rhy[r] *= imu; rez[r] *= ieps; }
-      }
-    }
-    if constexpr (MT::rk) {
-      T* __restrict__ res = static_cast<T*>(p.res);
-      T* __restrict__ qo = static_cast<T*>(p.q_out);
-      const T a = static_cast<T>(p.a), b = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
-#pragma unroll
-      for (int n = 0; n < NP; ++n) {
-        const int64_t off = ((int64_t)tile * NP + n) * TL + lane;
-        const T rhs[3] = {rhx[n], rhy[n], rez[n]};
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          T rs = dt * rhs[c];
-          if (read_res) rs = fmaf(a, rr[c][n], rs);
-          if (p.write_res) __stcs(res + c * p.vstride + off, rs);
-          __stcs(qo + c * p.fstride + off, fmaf(b, rs, sq[(c * NP + n) * TL + lane]));
-        }
-      }
-    } else {
-      T* __restrict__ out = static_cast<T*>(p.out);
-#pragma unroll
-      for (int n = 0; n < NP; ++n) {
-        const int64_t off = ((int64_t)tile * NP + n) * TL + lane;
-        out[off] = rhx[n];
-        out[p.vstride + off] = rhy[n];
-        out[2 * p.vstride + off] = rez[n];
-      }
-    }
-    __syncwarp();
-  }
-}
-
-template <int MODE, bool MAT>
-cudaError_t launch_one_w(const dg::StageArgs& a, cudaStream_t s) {
-  constexpr size_t smem = w_smem_total(MAT);
-  static int grid_cap[64] = {0};
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  if (dev >= 64) return cudaErrorInvalidDevice;
-  if (grid_cap[dev] == 0) {
-    e = cudaFuncSetAttribute(stage_kernel_w<MODE, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_kernel_w<MODE, MAT>, WPC * 32, smem);
-    if (e != cudaSuccess) return e;
-    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return e;
-    grid_cap[dev] = (per_sm > 0 ? per_sm : 1) * sms;
-  }
-  int grid = (a.ntiles + WPC - 1) / WPC;
-  if (grid > grid_cap[dev]) grid = grid_cap[dev];
-  if (grid <= 0) return cudaSuccess;
-  stage_kernel_w<MODE, MAT><<<grid, WPC * 32, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
 template <int MODE, bool MAT>
 cudaError_t launch_one(const dg::StageArgs& a, cudaStream_t s) {
-  if constexpr (USE_W) return launch_one_w<MODE, MAT>(a, s);
   using MT = ModeTraits<MODE>;
   constexpr size_t smem = smem_total(nslots(MT::surf, MAT, MT::rk), MT::surf, MAT, MT::rk);
   static int grid_cap[64] = {0};  // resident CTAs (whole GPU) per device ordinal
@@ -766,7 +538,7 @@ void pack_ops(const double* Dr, const double* Ds, const double* LIFT, void* out)
     for (int n = 0; n < RP; ++n)
       for (int k = 0; k < VC; ++k) {
         const int m = mc * VC + k;
-        if (n < NP && m < NF) lv[(size_t)(mc * RP + n) * VC + k] = static_cast<T>(LIFT[n * NF + m]);
+        if (n < NP && m < NF) lv[(size_t)(mc * RPL + n) * VC + k] = static_cast<T>(LIFT[n * NF + m]);
       }
 }
 

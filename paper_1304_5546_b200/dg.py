@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdg.so")
+LIB_PATH = os.environ.get("DG_LIB") or os.path.join(_HERE, "lib", "libdg.so")  # DG_LIB: dev override
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built; run `python -m paper_1304_5546_b200.build`")
