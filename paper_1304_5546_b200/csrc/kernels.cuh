@@ -74,7 +74,7 @@ constexpr int NFE = NFC * VC;            // padded face points per element (flux
 //   ops : DV[NPC][RP] (fp32 float4 {Dr_j, Ds_j, Dr_j+1, Ds_j+1} | fp64 double2 {Dr_j, Ds_j})
 //         LV[NFC][RP] (fp32 float2 {L_m, L_m+1} | fp64 double L_m)
 //   S slots of { q [3][NP][32], geo [NGEO][32], sp [3][NFE][32] }
-//   vm  [3][NF][32] int32 (vmapP of the next tiles),  res [3][NP][32]
+// (vmapP codes and the LSERK4 residual live in registers)
 constexpr size_t DVB = (size_t)NPC * RP * 2 * VC * sizeof(T);
 constexpr int RPL = (RP + 1) & ~1;  // LIFT rows padded to even
 constexpr size_t LVB = (size_t)NFC * RPL * VC * sizeof(T);
@@ -82,16 +82,24 @@ constexpr size_t OPB = ((DVB + LVB + 15) / 16) * 16;
 constexpr size_t QB = (size_t)3 * NP * TL * sizeof(T);
 __host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)(mat ? dg::NGEO_MAT : dg::NGEO_CONST) * TL * sizeof(T); }
 constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
-constexpr size_t VMB = (size_t)NF * TL * sizeof(int32_t);
 __host__ __device__ constexpr size_t slot_bytes(bool surf, bool mat) { return QB + geo_bytes(mat) + (surf ? SPB : 0); }
-constexpr size_t BARB = 64;  // mbarriers: one per slot + one for the residual buffer
-__host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat, bool rk) {
-  return BARB + OPB + S * slot_bytes(surf, mat) + (surf ? 3 * VMB : 0) + (rk ? QB : 0);
-}
-// double-buffer when two teams still fit on an SM, else single-buffer
-__host__ __device__ constexpr int nslots(bool surf, bool mat, bool rk) { return smem_total(2, surf, mat, rk) <= 113 * 1024 ? 2 : 1; }
-constexpr int CTAS_BY_SMEM = (int)((227 * 1024) / smem_total(nslots(true, false, true), true, false, true));
-constexpr int MIN_CTAS = CTAS_BY_SMEM < 1 ? 1 : (CTAS_BY_SMEM > 8 ? 8 : CTAS_BY_SMEM);
+constexpr size_t BARB = 64;  // mbarriers: one per slot
+__host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat) { return BARB + OPB + S * slot_bytes(surf, mat); }
+// slots per team: 2 (double-buffered: tile t+1 streams in while t computes) unless that
+// leaves fewer than 3 teams per SM, then 1 (latency hidden across teams instead)
+#ifndef DG_SLOTS
+// measured at C4 (N=5): fp32 is issue-bound and prefers more resident teams (1 slot),
+// fp64 is latency-bound and prefers the in-team double buffer (2 slots)
+__host__ __device__ constexpr int nslots(bool, bool) { return F32 ? 1 : 2; }
+#else
+__host__ __device__ constexpr int nslots(bool, bool) { return DG_SLOTS; }
+#endif
+constexpr int CTAS_BY_SMEM = (int)((227 * 1024) / smem_total(nslots(true, false), true, false));
+#ifndef DG_MAXCTAS
+#define DG_MAXCTAS 5  // measured (C4 fp32): 5 teams x 128 registers beats 8 x 80 (spills) and 4 x 168
+#endif
+constexpr int MIN_CTAS = CTAS_BY_SMEM < 1 ? 1 : (CTAS_BY_SMEM > DG_MAXCTAS ? DG_MAXCTAS : CTAS_BY_SMEM);
+constexpr int KPT = (NF + P - 1) / P;  // face points per thread (point m belongs to warp m % P)
 
 // Face node ids, increasing node index (closed form of the node ordering: row j
 // of the triangle starts at j(N+1) - j(j-1)/2).  Checked against the setup's
@@ -211,14 +219,17 @@ __device__ __forceinline__ void volume_rows(const T* __restrict__ sq, const DVT*
 // straight from the tile's shared-memory fields at offset -(1 + code).
 template <bool MAT>
 __device__ __forceinline__ void flux_points(const T* __restrict__ sq, const T* __restrict__ gg, T* __restrict__ sp,
-                                            const int32_t* __restrict__ vm, int g, int lane, T alpha) {
-  for (int m = g; m < NF; m += P) {
+                                            const int32_t (&vmc)[KPT], int g, int lane, T alpha) {
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int m = g + k * P;
+    if (m >= NF) break;
     const int f = m < NFP ? 0 : (m < 2 * NFP ? 1 : 2);
     const int i = m - f * NFP;
     const int fm = f == 0 ? i : (f == 1 ? row_start(i) + N - i : row_start(i));
     const T nx = gg[(4 + 3 * f) * TL], ny = gg[(5 + 3 * f) * TL], hF = gg[(6 + 3 * f) * TL];
     const T bsc = gg[(13 + f) * TL];
-    const int code = vm[m * TL + lane];
+    const int code = vmc[k];
     const T* pp = code < 0 ? sq + (-1 - code) : sp + m * TL + lane;  // neighbour trace, field 0
     const int fs = code < 0 ? NP * TL : NFE * TL;                     // field stride of that source
     const T dHx = sq[(0 * NP + fm) * TL + lane] - pp[0];
@@ -287,7 +298,7 @@ template <int MODE, bool MAT>
 __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageArgs p) {
   using MT = ModeTraits<MODE>;
   constexpr int NG = MAT ? dg::NGEO_MAT : dg::NGEO_CONST;
-  constexpr int S = nslots(MT::surf, MAT, MT::rk);
+  constexpr int S = nslots(MT::surf, MAT);
   constexpr size_t SLOT = slot_bytes(MT::surf, MAT);
   constexpr size_t GB = geo_bytes(MAT);
   constexpr int CH = 16 / (int)sizeof(T);
@@ -307,18 +318,23 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   auto sq_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT); };
   auto sg_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB); };
   auto sp_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB + GB); };
-  auto vm_of = [&](int v) { return reinterpret_cast<int32_t*>(slots + S * SLOT + v * VMB); };
-  T* const sr = reinterpret_cast<T*>(slots + S * SLOT + (MT::surf ? 3 * VMB : 0));
   const bool read_res = MT::rk && p.a != 0.0;
+  const int g = tid >> 5, lane = tid & 31;
 
   auto tile_of = [&](int it) {
     const int sidx = first + it * stride;
     return p.tiles ? p.tiles[sidx] : sidx;
   };
-  auto issue_vm = [&](int it) {
-    const int4* src = reinterpret_cast<const int4*>(p.vmapP + (int64_t)tile_of(it) * NF * TL);
-    int4* dst = reinterpret_cast<int4*>(vm_of(it % 3));
-    for (int i = tid; i < NF * TL / 4; i += TEAM) cp_async16(dst + i, src + i);
+  // vmapP codes of this thread's face points (m = g + k P) of tile `it`
+  auto load_codes = [&](int it, int32_t (&v)[KPT]) {
+    if constexpr (MT::surf) {
+      const int32_t* src = p.vmapP + (int64_t)tile_of(it) * NF * TL + lane;
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        const int m = g + k * P;
+        v[k] = m < NF ? __ldg(src + m * TL) : -1;
+      }
+    }
   };
   // fields + geometry of tile `it`: four TMA bulk copies issued by one thread
   auto issue_tma = [&](int it) {
@@ -334,24 +350,25 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       tma_load_1d(sg_of(s), geo + (int64_t)tile * NG * TL, (unsigned)GB, bar);
     }
   };
-  // neighbour traces of tile `it` (needs its vmapP in vm[it % 3])
-  auto issue_gather = [&](int it) {
+  // cross-tile neighbour traces of tile `it` (same-tile ones are read from shared memory)
+  auto issue_gather = [&](int it, const int32_t (&v)[KPT]) {
     if constexpr (MT::surf) {
-      const int32_t* v = vm_of(it % 3) + (tid & 31);
-      T* sp = sp_of(it % S) + (tid & 31);
-      for (int m = tid >> 5; m < NF; m += P) {
-        const int code = v[m * TL];
-        if (code < 0) continue;  // same-tile neighbour: read from shared memory in the flux phase
-        const T* src = q + code;
+      T* sp = sp_of(it % S) + lane;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) cp_async_small<sizeof(T)>(sp + (c * NFE + m) * TL, src + c * p.fstride);
+      for (int k = 0; k < KPT; ++k) {
+        const int m = g + k * P;
+        if (m < NF && v[k] >= 0) {
+          const T* src = q + v[k];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) cp_async_small<sizeof(T)>(sp + (c * NFE + m) * TL, src + c * p.fstride);
+        }
       }
     }
   };
 
   // prologue: barriers, operators (once per persistent CTA), zero flux pad columns, first tiles
   if (tid == 0) {
-    for (int b = 0; b <= S; ++b) mbar_init(bars + b, 1);
+    for (int b = 0; b < S; ++b) mbar_init(bars + b, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   {
@@ -367,37 +384,30 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       }
     }
   }
-  if constexpr (MT::surf) issue_vm(0);
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
+  int32_t vc0[KPT], vc1[KPT], vc2[KPT];  // codes of tiles it, it+1, it+2
+  load_codes(0, vc0);
+  if (n_it > 1) load_codes(1, vc1);
   issue_tma(0);
-  issue_gather(0);
-  if (MT::surf && n_it > 1) issue_vm(1);
+  issue_gather(0, vc0);
   cp_async_commit();
 
-  const int g = tid >> 5, lane = tid & 31;
   const int n0 = g * R;
   const T alpha = static_cast<T>(p.alpha);
   for (int it = 0; it < n_it; ++it) {
     const int s = it % S;
-    cp_async_wait_all();                     // gathers of tile it, vmapP of tile it+1
+    cp_async_wait_all();                            // gathers of tile it
     mbar_wait(bars + s, (unsigned)((it / S) & 1));  // TMA: fields + geometry of tile it
     __syncthreads();
     const int tile = tile_of(it);
-    if (read_res && tid == 0) {  // this tile's residual, consumed in the epilogue
-      mbar_expect_tx(bars + S, (unsigned)QB);
-      const T* __restrict__ res = static_cast<const T*>(p.res);
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-        tma_load_1d(sr + c * NP * TL, res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bars + S);
-    }
     if (S == 2 && it + 1 < n_it) {
       issue_tma(it + 1);
-      issue_gather(it + 1);
-      if (MT::surf && it + 2 < n_it) issue_vm(it + 2);
+      issue_gather(it + 1, vc1);
       cp_async_commit();
     }
+    if (it + 2 < n_it) load_codes(it + 2, vc2);
 
     const T* sq = sq_of(s);
     const T* gg = sg_of(s) + lane;
@@ -419,8 +429,21 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
 #pragma unroll
       for (int r = 0; r < R; ++r) { rhx[r] = T(0); rhy[r] = T(0); rez[r] = T(0); }
     }
+    // LSERK4 residual of this tile -> registers (in flight during the surface phase)
+    T rr[3][R];
+    if constexpr (MT::rk) {
+      if (read_res) {
+        const T* __restrict__ res = static_cast<const T*>(p.res);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int n = n0 + r < NP ? n0 + r : NP - 1;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) rr[c][r] = __ldcs(res + c * p.vstride + ((int64_t)tile * NP + n) * TL + lane);
+        }
+      }
+    }
     if constexpr (MT::surf) {
-      flux_points<MAT>(sq, gg, sp, vm_of(it % 3), g, lane, alpha);
+      flux_points<MAT>(sq, gg, sp, vc0, g, lane, alpha);
       __syncthreads();
       lift_rows(sp, LV, n0, lane, rhx, rhy, rez);
     }
@@ -437,7 +460,6 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       T* __restrict__ res = static_cast<T*>(p.res);
       T* __restrict__ qo = static_cast<T*>(p.q_out);
       const T a = static_cast<T>(p.a), b = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
-      if (read_res) mbar_wait(bars + S, (unsigned)(it & 1));
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int n = n0 + r;
@@ -447,7 +469,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           T rs = dt * rhs[c];
-          if (read_res) rs = fma(a, sr[(c * NP + n) * TL + lane], rs);
+          if (read_res) rs = fma(a, rr[c][r], rs);
           if (p.write_res) __stcs(res + c * p.vstride + off, rs);
           __stcs(qo + c * p.fstride + off, fma(b, rs, sq[(c * NP + n) * TL + lane]));
         }
@@ -467,17 +489,18 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     if (S == 1 && it + 1 < n_it) {
       __syncthreads();
       issue_tma(it + 1);
-      issue_gather(it + 1);
-      if (MT::surf && it + 2 < n_it) issue_vm(it + 2);
+      issue_gather(it + 1, vc1);
       cp_async_commit();
     }
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) { vc0[k] = vc1[k]; vc1[k] = vc2[k]; }
   }
 }
 
 template <int MODE, bool MAT>
 cudaError_t launch_one(const dg::StageArgs& a, cudaStream_t s) {
   using MT = ModeTraits<MODE>;
-  constexpr size_t smem = smem_total(nslots(MT::surf, MAT, MT::rk), MT::surf, MAT, MT::rk);
+  constexpr size_t smem = smem_total(nslots(MT::surf, MAT), MT::surf, MAT);
   static int grid_cap[64] = {0};  // resident CTAs (whole GPU) per device ordinal
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -555,10 +578,10 @@ dg::KernelInfo info() {
   k.N = N;
   k.prec = (int)sizeof(T);
   k.threads = TEAM;
-  k.slots = nslots(true, false, true);
+  k.slots = nslots(true, false);
   k.row_groups = P;
   k.rows_per_group = R;
-  k.smem_bytes = smem_total(nslots(true, false, true), true, false, true);
+  k.smem_bytes = smem_total(nslots(true, false), true, false);
   return k;
 }
 
