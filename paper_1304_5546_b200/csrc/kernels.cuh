@@ -51,14 +51,15 @@ constexpr int NFP = N + 1;
 constexpr int NF = 3 * NFP;
 constexpr int TL = dg::TILE;
 
-// rows per warp and team size (a team of P warps shares each tile)
-#ifndef DG_RMAX32
-#define DG_RMAX32 8
+// Tuning knobs (per (N, precision) from csrc/tune.json via build.py; defaults
+// below were measured at C4, N=5):
+//   DG_R  max output rows per warp  -> team size P = ceil(Np / R)
+//   DG_S  shared-memory slots per team (1 or 2)
+//   DG_C  cap on resident teams per SM (sets the register budget via launch bounds)
+#ifndef DG_R
+#define DG_R (sizeof(DG_T) == 4 ? 8 : 6)
 #endif
-#ifndef DG_RMAX64
-#define DG_RMAX64 6
-#endif
-constexpr int R_TARGET = F32 ? DG_RMAX32 : DG_RMAX64;  // max rows per warp
+constexpr int R_TARGET = DG_R;  // max rows per warp
 constexpr int P = (NP + R_TARGET - 1) / R_TARGET;     // warps per tile
 constexpr int R = (NP + P - 1) / P;                // rows per warp
 constexpr int RP = P * R;                          // padded rows (extra rows are zero)
@@ -85,20 +86,18 @@ constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
 __host__ __device__ constexpr size_t slot_bytes(bool surf, bool mat) { return QB + geo_bytes(mat) + (surf ? SPB : 0); }
 constexpr size_t BARB = 64;  // mbarriers: one per slot
 __host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat) { return BARB + OPB + S * slot_bytes(surf, mat); }
-// slots per team: 2 (double-buffered: tile t+1 streams in while t computes) unless that
-// leaves fewer than 3 teams per SM, then 1 (latency hidden across teams instead)
-#ifndef DG_SLOTS
-// measured at C4 (N=5): fp32 is issue-bound and prefers more resident teams (1 slot),
-// fp64 is latency-bound and prefers the in-team double buffer (2 slots)
-__host__ __device__ constexpr int nslots(bool, bool) { return F32 ? 1 : 2; }
-#else
-__host__ __device__ constexpr int nslots(bool, bool) { return DG_SLOTS; }
+// Slots per team: 2 = double-buffered (tile t+1 streams in while t computes), 1 = latency
+// hidden across resident teams instead.  Measured at C4 (N=5): fp32 is issue-bound and
+// prefers more resident teams (1 slot), fp64 is latency-bound and prefers 2 slots.
+#ifndef DG_S
+#define DG_S (sizeof(DG_T) == 4 ? 1 : 2)
 #endif
+__host__ __device__ constexpr int nslots(bool, bool) { return DG_S; }
 constexpr int CTAS_BY_SMEM = (int)((227 * 1024) / smem_total(nslots(true, false), true, false));
-#ifndef DG_MAXCTAS
-#define DG_MAXCTAS 5  // measured (C4 fp32): 5 teams x 128 registers beats 8 x 80 (spills) and 4 x 168
+#ifndef DG_C
+#define DG_C 5  // measured (C4 fp32): 5 teams x 128 registers beats 8 x 80 (spills) and 4 x 168
 #endif
-constexpr int MIN_CTAS = CTAS_BY_SMEM < 1 ? 1 : (CTAS_BY_SMEM > DG_MAXCTAS ? DG_MAXCTAS : CTAS_BY_SMEM);
+constexpr int MIN_CTAS = CTAS_BY_SMEM < 1 ? 1 : (CTAS_BY_SMEM > DG_C ? DG_C : CTAS_BY_SMEM);
 constexpr int KPT = (NF + P - 1) / P;  // face points per thread (point m belongs to warp m % P)
 
 // Face node ids, increasing node index (closed form of the node ordering: row j
@@ -523,6 +522,10 @@ cudaError_t launch_one(const dg::StageArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch(int mode, bool mat, const dg::StageArgs& a, cudaStream_t s) {
+#ifdef DG_TUNE_ONLY  // autotuning builds: only the fused constant-material kernel
+  if (mode == dg::MODE_FUSED_RK && !mat) return launch_one<dg::MODE_FUSED_RK, false>(a, s);
+  return cudaErrorNotSupported;
+#else
   switch (mode * 2 + (mat ? 1 : 0)) {
     case dg::MODE_FUSED_RK * 2 + 0: return launch_one<dg::MODE_FUSED_RK, false>(a, s);
     case dg::MODE_FUSED_RK * 2 + 1: return launch_one<dg::MODE_FUSED_RK, true>(a, s);
@@ -536,6 +539,7 @@ cudaError_t launch(int mode, bool mat, const dg::StageArgs& a, cudaStream_t s) {
     case dg::MODE_SURFACE * 2 + 1: return launch_one<dg::MODE_SURFACE, true>(a, s);
     default: return cudaErrorInvalidValue;
   }
+#endif
 }
 
 // Host: pack Dr, Ds [Np][Np] and LIFT [Np][3Nfp] (fp64, row-major) into the

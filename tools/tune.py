@@ -1,0 +1,124 @@
+"""Autotuning of the stage-kernel knobs per (N, precision) -- the paper's
+"looping over all variants and comparing timing data for each".
+
+    python tools/tune.py build            # CPU: build one library per knob set -> build_variants/
+    python tools/tune.py measure OUT.json # GPU: time the fused stage for every (variant, N, precision)
+    python tools/tune.py pick OUT.json    # CPU: write paper_1304_5546_b200/csrc/tune.json
+
+Knobs: R (max rows per warp -> team size), S (shared-memory slots), C (teams/SM cap).
+Timing: one LSERK4 stage = one fused launch, CUDA events, mean of 5 steps after warm-up,
+on an n x n A16 mesh (default n=362, K=262,088).  Every variant's result is checked
+against the default build's fields after the run (identical arithmetic => bitwise).
+"""
+import itertools
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VDIR = os.path.join(ROOT, "build_variants")
+
+GRID = {
+    4: [dict(R=r, S=s, C=c) for r, s, c in itertools.product((6, 8, 11), (1, 2), (3, 5))],
+    8: [dict(R=r, S=s, C=c) for r, s, c in itertools.product((4, 6, 8), (1, 2), (3, 5))],
+}
+
+
+def name_of(k):
+    return f"R{k['R']}_S{k['S']}_C{k['C']}"
+
+
+def cmd_build():
+    from paper_1304_5546_b200 import build as B
+
+    knobsets = {name_of(k): k for ks in GRID.values() for k in ks}
+    for nm, k in sorted(knobsets.items()):
+        lib = B.build_variant(nm, k, VDIR)
+        print(lib, flush=True)
+
+
+def cmd_measure(out):
+    import numpy as np
+    import torch
+
+    import dginputs
+
+    n = int(os.environ.get("TUNE_N", "362"))
+    VX, VY, E = dginputs.rect_mesh(n)
+    results = []
+    libs = sorted(f for f in os.listdir(VDIR) if f.endswith(".so"))
+    # each variant in a fresh process (one libdg.so per process)
+    import subprocess
+
+    for lib in libs:
+        code = f"""
+import sys, json; sys.path.insert(0, {ROOT!r})
+import numpy as np, torch, dginputs
+from paper_1304_5546_b200 import dg
+VX, VY, E = dginputs.rect_mesh({n})
+out = []
+for N in range(1, 10):
+    dt = dginputs.cfl_dt(VX, VY, E, N)
+    for prec in (4, 8):
+        try:
+            c = dg.dg_setup(N, VX, VY, E, precision=prec)
+        except dg.DGError as e:
+            continue
+        x, y = c.nodes()
+        c.set_fields(*dginputs.cavity_mode(x, y, 0.0))
+        c.run(dt, 3); c.sync()
+        s = torch.cuda.ExternalStream(c.stream())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s); c.run(dt, 5); e1.record(s); e1.synchronize()
+        ms = e0.elapsed_time(e1) / 25
+        f = c.get_fields()
+        out.append(dict(N=N, prec=prec, ms=ms, chk=float(sum(np.abs(a).sum() for a in f))))
+        c.destroy()
+print(json.dumps(out))
+"""
+        env = dict(os.environ, DG_LIB=os.path.join(VDIR, lib))
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env)
+        if p.returncode != 0:
+            print(lib, "FAILED", p.stderr[-500:], flush=True)
+            continue
+        rows = json.loads(p.stdout.strip().splitlines()[-1])
+        for r in rows:
+            r["variant"] = lib[:-3]
+        results += rows
+        print(lib, " ".join(f"N{r['N']}p{r['prec']}:{r['ms']:.4f}" for r in rows), flush=True)
+    with open(out, "w") as fh:
+        json.dump(dict(n=n, results=results), fh, indent=1)
+
+
+def cmd_pick(path):
+    d = json.load(open(path))
+    best = {}
+    chk = {}
+    for r in d["results"]:
+        key = f"N{r['N']}_{'f32' if r['prec'] == 4 else 'f64'}"
+        chk.setdefault(key, r["chk"])
+        if abs(r["chk"] - chk[key]) > 1e-6 * abs(chk[key]):
+            print("WARNING: checksum mismatch", key, r["variant"])
+            continue
+        if key not in best or r["ms"] < best[key]["ms"]:
+            best[key] = r
+    tune = {"_doc": f"picked by tools/tune.py from {os.path.basename(path)} (fused stage, "
+                    f"{d['n']}x{d['n']} A16 mesh): fastest knob set per (N, precision)"}
+    for key, r in sorted(best.items()):
+        k = dict(kv.split(":") for kv in [])
+        R, S, C = (int(x[1:]) for x in r["variant"].split("_"))
+        tune[key] = dict(R=R, S=S, C=C, ms=round(r["ms"], 5))
+    out = os.path.join(ROOT, "paper_1304_5546_b200", "csrc", "tune.json")
+    with open(out, "w") as fh:
+        json.dump(tune, fh, indent=1)
+    print(json.dumps(tune, indent=1))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        cmd_build()
+    elif sys.argv[1] == "measure":
+        cmd_measure(sys.argv[2])
+    elif sys.argv[1] == "pick":
+        cmd_pick(sys.argv[2])
