@@ -70,6 +70,9 @@ struct KernelModule {
   cudaError_t (*launch)(int mode, bool material, const StageArgs& a, cudaStream_t s) = nullptr;
   KernelInfo (*info)() = nullptr;
   bool (*check_fmask)(const int* Fmask) = nullptr;
+  // column swizzle of the tile-blocked layout: element `lane` of node row n lives at
+  // column lane ^ (swizzle * (n & 3)) (0 = plain layout)
+  int swizzle = 0;
 };
 
 // Registry: one entry per compiled (N, prec); nullptr if not compiled.

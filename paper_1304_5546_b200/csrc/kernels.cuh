@@ -56,10 +56,16 @@ constexpr int TL = dg::TILE;
 //   DG_R  max output rows per warp  -> team size P = ceil(Np / R)
 //   DG_S  shared-memory slots per team (1 or 2)
 //   DG_C  cap on resident teams per SM (sets the register budget via launch bounds)
+//   DG_MMA fp64 only: volume and LIFT contractions on the FP64 tensor cores (DMMA,
+//          mma.sync m8n8k4) -- one 8-row m-tile per warp -- instead of DFMA
+#ifndef DG_MMA
+#define DG_MMA 0  // chosen per (N, precision) by tools/tune.py
+#endif
+constexpr bool USE_MMA = !F32 && DG_MMA;
 #ifndef DG_R
 #define DG_R (sizeof(DG_T) == 4 ? 8 : 6)
 #endif
-constexpr int R_TARGET = DG_R;  // max rows per warp
+constexpr int R_TARGET = USE_MMA ? 8 : DG_R;  // max rows per warp
 constexpr int P = (NP + R_TARGET - 1) / R_TARGET;     // warps per tile
 constexpr int R = (NP + P - 1) / P;                // rows per warp
 constexpr int RP = P * R;                          // padded rows (extra rows are zero)
@@ -76,10 +82,19 @@ constexpr int NFE = NFC * VC;            // padded face points per element (flux
 //         LV[NFC][RP] (fp32 float2 {L_m, L_m+1} | fp64 double L_m)
 //   S slots of { q [3][NP][32], geo [NGEO][32], sp [3][NFE][32] }
 // (vmapP codes and the LSERK4 residual live in registers)
-constexpr size_t DVB = (size_t)NPC * RP * 2 * VC * sizeof(T);
+//   MMA ops (fp64): AV[KV][P][32] double2 {Dr, Ds} and AL[KL][P][32] double LIFT, each lane
+//         holding its m8n8k4 A-fragment element (row 8g + lane/4, column 4k + lane%4)
+constexpr int KV = (NP + 3) / 4;  // MMA k-steps of the volume contraction
+constexpr int KL = (NF + 3) / 4;  // MMA k-steps of the LIFT contraction
+constexpr size_t DVB = USE_MMA ? (size_t)KV * P * 32 * 16 : (size_t)NPC * RP * 2 * VC * sizeof(T);
 constexpr int RPL = (RP + 1) & ~1;  // LIFT rows padded to even
-constexpr size_t LVB = (size_t)NFC * RPL * VC * sizeof(T);
+constexpr size_t LVB = USE_MMA ? (size_t)KL * P * 32 * 8 : (size_t)NFC * RPL * VC * sizeof(T);
 constexpr size_t OPB = ((DVB + LVB + 15) / 16) * 16;
+// Column swizzle of the tile-blocked layout: element e of node row n is stored at
+// column e ^ (SWM * (n & 3)).  Identity for the FMA kernels; for the DMMA kernels
+// it makes the B-fragment loads (4 rows x 8 elements) bank-conflict free.
+constexpr int SWM = USE_MMA ? 4 : 0;
+__host__ __device__ constexpr int colx(int n, int e) { return e ^ (SWM * (n & 3)); }
 constexpr size_t QB = (size_t)3 * NP * TL * sizeof(T);
 __host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)(mat ? dg::NGEO_MAT : dg::NGEO_CONST) * TL * sizeof(T); }
 constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
@@ -229,11 +244,13 @@ __device__ __forceinline__ void flux_points(const T* __restrict__ sq, const T* _
     const T nx = gg[(4 + 3 * f) * TL], ny = gg[(5 + 3 * f) * TL], hF = gg[(6 + 3 * f) * TL];
     const T bsc = gg[(13 + f) * TL];
     const int code = vmc[k];
-    const T* pp = code < 0 ? sq + (-1 - code) : sp + m * TL + lane;  // neighbour trace, field 0
+    const int pm = m * TL + colx(m, lane);                            // this point in sp
+    const T* pp = code < 0 ? sq + (-1 - code) : sp + pm;              // neighbour trace, field 0
     const int fs = code < 0 ? NP * TL : NFE * TL;                     // field stride of that source
-    const T dHx = sq[(0 * NP + fm) * TL + lane] - pp[0];
-    const T dHy = sq[(1 * NP + fm) * TL + lane] - pp[fs];
-    const T dEz = sq[(2 * NP + fm) * TL + lane] - bsc * pp[2 * fs];
+    const int om = fm * TL + colx(fm, lane);                          // own face node in sq
+    const T dHx = sq[0 * NP * TL + om] - pp[0];
+    const T dHy = sq[1 * NP * TL + om] - pp[fs];
+    const T dEz = sq[2 * NP * TL + om] - bsc * pp[2 * fs];
     T fHx, fHy, fEz;
     if constexpr (!MAT) {
       const T ndotdH = nx * dHx + ny * dHy;
@@ -249,9 +266,73 @@ __device__ __forceinline__ void flux_points(const T* __restrict__ sq, const T* _
       fHy = -hF * (nx * gH);
       fEz = -hF * (wHE * dHt + wEE * dEz);
     }
-    sp[(0 * NFE + m) * TL + lane] = fHx;
-    sp[(1 * NFE + m) * TL + lane] = fHy;
-    sp[(2 * NFE + m) * TL + lane] = fEz;
+    sp[0 * NFE * TL + pm] = fHx;
+    sp[1 * NFE * TL + pm] = fHy;
+    sp[2 * NFE * TL + pm] = fEz;
+  }
+}
+
+// ---------------------------------------------------------------- DMMA (fp64 tensor core) path
+// D(8x8) += A(8x4) B(4x8), fp64: lane holds A[lane/4][lane%4], B[lane%4][lane/4],
+// C[lane/4][2(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// Volume term of one tile on the tensor cores: warp g owns rows [8g, 8g+8), the
+// four 8-element n-tiles of the tile are the columns.  u = Dr Ez, v = Ds Ez,
+// w = Dr W1 + Ds W2 with W1 = rx Hy - ry Hx, W2 = sx Hy - sy Hx per element
+// (same algebra as volume_rows), accumulated over KV k-steps of 4 nodes.
+template <typename AVT>
+__device__ __forceinline__ void volume_mma(const double* __restrict__ sq, const double* __restrict__ sg,
+                                           const AVT* __restrict__ AV, int g, int lane, double (&u)[4][2],
+                                           double (&v)[4][2], double (&w)[4][2]) {
+  double rxb[4], sxb[4], ryb[4], syb[4];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const int eb = 8 * nt + (lane >> 2);
+    rxb[nt] = sg[0 * TL + eb];
+    sxb[nt] = sg[1 * TL + eb];
+    ryb[nt] = sg[2 * TL + eb];
+    syb[nt] = sg[3 * TL + eb];
+    u[nt][0] = u[nt][1] = v[nt][0] = v[nt][1] = w[nt][0] = w[nt][1] = 0.0;
+  }
+#pragma unroll
+  for (int ks = 0; ks < KV; ++ks) {
+    const int j = 4 * ks + (lane & 3);
+    const int jc = j < NP ? j : NP - 1;  // padded k rows: A is zero there
+    const AVT a = AV[(ks * P + g) * 32 + lane];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int addr = jc * TL + colx(jc, 8 * nt + (lane >> 2));
+      const double hx = sq[0 * NP * TL + addr], hy = sq[1 * NP * TL + addr], ez = sq[2 * NP * TL + addr];
+      const double w1 = rxb[nt] * hy - ryb[nt] * hx;
+      const double w2 = sxb[nt] * hy - syb[nt] * hx;
+      dmma(u[nt][0], u[nt][1], a.x, ez);
+      dmma(v[nt][0], v[nt][1], a.y, ez);
+      dmma(w[nt][0], w[nt][1], a.x, w1);
+      dmma(w[nt][0], w[nt][1], a.y, w2);
+    }
+  }
+}
+
+// rhs += LIFT f on the tensor cores (f in sp, swizzled [c][NF][32]).
+__device__ __forceinline__ void lift_mma(const double* __restrict__ sp, const double* __restrict__ AL, int g,
+                                         int lane, double (&rhx)[4][2], double (&rhy)[4][2], double (&rez)[4][2]) {
+#pragma unroll
+  for (int ks = 0; ks < KL; ++ks) {
+    const int m = 4 * ks + (lane & 3);
+    const int mc = m < NF ? m : NF - 1;
+    const double a = AL[(ks * P + g) * 32 + lane];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int addr = mc * TL + colx(mc, 8 * nt + (lane >> 2));
+      dmma(rhx[nt][0], rhx[nt][1], a, sp[0 * NFE * TL + addr]);
+      dmma(rhy[nt][0], rhy[nt][1], a, sp[1 * NFE * TL + addr]);
+      dmma(rez[nt][0], rez[nt][1], a, sp[2 * NFE * TL + addr]);
+    }
   }
 }
 
@@ -287,6 +368,122 @@ __device__ __forceinline__ void lift_rows(const T* __restrict__ sp, const LVT* _
         rhx[r] = fma(l, a0, rhx[r]);
         rhy[r] = fma(l, b0, rhy[r]);
         rez[r] = fma(l, c0, rez[r]);
+      }
+    }
+  }
+}
+
+// One tile on the DMMA path (fp64): volume (tensor cores) -> flux (one lane per
+// element, as the FMA path) -> LIFT (tensor cores) -> material scaling -> LSERK4
+// update.  Each lane owns C-fragment rows n = 8g + lane/4 and the element pairs
+// e = 8nt + 2(lane%4) + {0,1}; stores are 16 B pairs (e, e+1 stay adjacent under
+// the column swizzle).
+template <int MODE, bool MAT, typename TT>
+__device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
+                                         TT* __restrict__ sp, const unsigned char* __restrict__ ops,
+                                         const int32_t (&vmc)[KPT], int tile, int g, int lane, TT alpha,
+                                         bool read_res) {
+  using MT = ModeTraits<MODE>;
+  using V2 = typename std::conditional<sizeof(TT) == 8, double2, float2>::type;
+  const int n = 8 * g + (lane >> 2);  // this lane's output row
+  const int nc = n < NP ? n : NP - 1;
+  TT rhx[4][2], rhy[4][2], rez[4][2];
+  if constexpr (MT::vol) {
+    TT u[4][2], v[4][2];
+    volume_mma(sq, sg, reinterpret_cast<const V2*>(ops), g, lane, u, v, rez);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int ec = 8 * nt + 2 * (lane & 3) + h;
+        const TT rx = sg[0 * TL + ec], sx = sg[1 * TL + ec], ry = sg[2 * TL + ec], sy = sg[3 * TL + ec];
+        rhx[nt][h] = -(ry * u[nt][h] + sy * v[nt][h]);
+        rhy[nt][h] = rx * u[nt][h] + sx * v[nt][h];
+      }
+  } else if constexpr (MODE == dg::MODE_SURFACE_RK) {
+    const TT* __restrict__ rv = static_cast<const TT*>(p.rhsv);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int64_t off = ((int64_t)tile * NP + nc) * TL + colx(nc, 8 * nt + 2 * (lane & 3));
+      const V2 x = *reinterpret_cast<const V2*>(rv + off);
+      const V2 y = *reinterpret_cast<const V2*>(rv + p.vstride + off);
+      const V2 z = *reinterpret_cast<const V2*>(rv + 2 * p.vstride + off);
+      rhx[nt][0] = x.x; rhx[nt][1] = x.y;
+      rhy[nt][0] = y.x; rhy[nt][1] = y.y;
+      rez[nt][0] = z.x; rez[nt][1] = z.y;
+    }
+  } else {
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) rhx[nt][h] = rhy[nt][h] = rez[nt][h] = TT(0);
+  }
+  // LSERK4 residual pairs -> registers (in flight during the surface phase)
+  V2 rr[3][4];
+  if constexpr (MT::rk) {
+    if (read_res) {
+      const TT* __restrict__ res = static_cast<const TT*>(p.res);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int64_t off = ((int64_t)tile * NP + nc) * TL + colx(nc, 8 * nt + 2 * (lane & 3));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) rr[c][nt] = __ldcs(reinterpret_cast<const V2*>(res + c * p.vstride + off));
+      }
+    }
+  }
+  if constexpr (MT::surf) {
+    flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
+    __syncthreads();
+    lift_mma(sp, reinterpret_cast<const TT*>(ops + DVB), g, lane, rhx, rhy, rez);
+  }
+  if constexpr (MAT) {
+    if (MODE != dg::MODE_VOLUME || p.scale_volume) {
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int ec = 8 * nt + 2 * (lane & 3) + h;
+          const TT imu = sg[16 * TL + ec], ieps = sg[17 * TL + ec];
+          rhx[nt][h] *= imu;
+          rhy[nt][h] *= imu;
+          rez[nt][h] *= ieps;
+        }
+    }
+  }
+  if (n >= NP) return;
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const int col = colx(n, 8 * nt + 2 * (lane & 3));
+    const int64_t off = ((int64_t)tile * NP + n) * TL + col;
+    const TT r3[3][2] = {{rhx[nt][0], rhx[nt][1]}, {rhy[nt][0], rhy[nt][1]}, {rez[nt][0], rez[nt][1]}};
+    if constexpr (MT::rk) {
+      TT* __restrict__ res = static_cast<TT*>(p.res);
+      TT* __restrict__ qo = static_cast<TT*>(p.q_out);
+      const TT a = static_cast<TT>(p.a), b = static_cast<TT>(p.b), dt = static_cast<TT>(p.dt);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        V2 rs;
+        rs.x = dt * r3[c][0];
+        rs.y = dt * r3[c][1];
+        if (read_res) {
+          rs.x = fma(a, rr[c][nt].x, rs.x);
+          rs.y = fma(a, rr[c][nt].y, rs.y);
+        }
+        if (p.write_res) __stcs(reinterpret_cast<V2*>(res + c * p.vstride + off), rs);
+        const V2 qi = *reinterpret_cast<const V2*>(sq + (c * NP + n) * TL + col);
+        V2 qn;
+        qn.x = fma(b, rs.x, qi.x);
+        qn.y = fma(b, rs.y, qi.y);
+        __stcs(reinterpret_cast<V2*>(qo + c * p.fstride + off), qn);
+      }
+    } else {
+      TT* __restrict__ out = static_cast<TT*>(p.out);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        V2 o;
+        o.x = r3[c][0];
+        o.y = r3[c][1];
+        *reinterpret_cast<V2*>(out + c * p.vstride + off) = o;
       }
     }
   }
@@ -358,8 +555,9 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
         const int m = g + k * P;
         if (m < NF && v[k] >= 0) {
           const T* src = q + v[k];
+          T* dst = sp - lane + m * TL + colx(m, lane);
 #pragma unroll
-          for (int c = 0; c < 3; ++c) cp_async_small<sizeof(T)>(sp + (c * NFE + m) * TL, src + c * p.fstride);
+          for (int c = 0; c < 3; ++c) cp_async_small<sizeof(T)>(dst + c * NFE * TL, src + c * p.fstride);
         }
       }
     }
@@ -411,6 +609,9 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     const T* sq = sq_of(s);
     const T* gg = sg_of(s) + lane;
     T* sp = sp_of(s);
+    if constexpr (USE_MMA) {
+      mma_tile<MODE, MAT>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, lane, alpha, read_res);
+    } else {
     T rhx[R], rhy[R], rez[R];
     if constexpr (MT::vol) {
       volume_rows(sq, DV, n0, lane, gg[0 * TL], gg[1 * TL], gg[2 * TL], gg[3 * TL], rhx, rhy, rez);
@@ -485,6 +686,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
         out[2 * p.vstride + off] = rez[r];
       }
     }
+    }  // !USE_MMA
     if (S == 1 && it + 1 < n_it) {
       __syncthreads();
       issue_tma(it + 1);
@@ -549,6 +751,27 @@ size_t ops_bytes() { return OPB; }
 void pack_ops(const double* Dr, const double* Ds, const double* LIFT, void* out) {
   unsigned char* o = static_cast<unsigned char*>(out);
   for (size_t i = 0; i < OPB; ++i) o[i] = 0;
+  if constexpr (USE_MMA) {  // A fragments: lane -> (row 8g + lane/4, column 4k + lane%4)
+    T* av = reinterpret_cast<T*>(o);
+    T* al = reinterpret_cast<T*>(o + DVB);
+    for (int g = 0; g < P; ++g)
+      for (int ln = 0; ln < 32; ++ln) {
+        const int n = 8 * g + ln / 4;
+        for (int ks = 0; ks < KV; ++ks) {
+          const int j = 4 * ks + ln % 4;
+          T* e = av + ((size_t)(ks * P + g) * 32 + ln) * 2;
+          if (n < NP && j < NP) {
+            e[0] = static_cast<T>(Dr[n * NP + j]);
+            e[1] = static_cast<T>(Ds[n * NP + j]);
+          }
+        }
+        for (int ks = 0; ks < KL; ++ks) {
+          const int m = 4 * ks + ln % 4;
+          if (n < NP && m < NF) al[(size_t)(ks * P + g) * 32 + ln] = static_cast<T>(LIFT[n * NF + m]);
+        }
+      }
+    return;
+  }
   T* dv = reinterpret_cast<T*>(o);
   for (int jc = 0; jc < NPC; ++jc)
     for (int n = 0; n < RP; ++n)
@@ -601,6 +824,7 @@ KernelModule DG_CAT(dg_module_, DG_TAG)() {
   m.launch = &launch;
   m.info = &info;
   m.check_fmask = &check_fmask;
+  m.swizzle = SWM;
   return m;
 }
 }  // namespace dg

@@ -97,17 +97,18 @@ Nccl* nccl() {
 // canonical fp64 [3][Kl][Np]  <->  tile-blocked T [3][fstride].  Device slot d
 // (tile d/32, lane d%32) holds local element perm[d] (-1: padding);
 // slot_of[kl] is the inverse.
+// (column swizzle swm: element `lane` of node row n sits at column lane ^ (swm * (n & 3)))
 template <typename T>
 __global__ void to_blocked(const double* __restrict__ src, T* __restrict__ q, const int32_t* __restrict__ perm,
-                           int64_t Kl, int64_t Kpad, int Np, int64_t fstride) {
+                           int64_t Kl, int64_t Kpad, int Np, int64_t fstride, int swm) {
   const int64_t total = Kpad * Np;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i / total);
-    const int64_t o = i - c * total;           // blocked offset within field: (t*Np + n)*32 + lane
-    const int lane = (int)(o & 31);
+    const int64_t o = i - c * total;           // blocked offset within field: (t*Np + n)*32 + column
     const int64_t tn = o >> 5;
     const int64_t t = tn / Np;
     const int n = (int)(tn - t * Np);
+    const int lane = (int)(o & 31) ^ (swm * (n & 3));
     const int64_t kl = perm[t * 32 + lane];
     q[c * fstride + o] = (kl >= 0) ? static_cast<T>(src[(c * Kl + kl) * Np + n]) : T(0);
   }
@@ -115,7 +116,7 @@ __global__ void to_blocked(const double* __restrict__ src, T* __restrict__ q, co
 
 template <typename T>
 __global__ void from_blocked(const T* __restrict__ q, double* __restrict__ dst, const int32_t* __restrict__ slot_of,
-                             int64_t Kl, int Np, int64_t fstride) {
+                             int64_t Kl, int Np, int64_t fstride, int swm) {
   const int64_t total = Kl * Np;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i / total);
@@ -123,7 +124,8 @@ __global__ void from_blocked(const T* __restrict__ q, double* __restrict__ dst, 
     const int64_t kl = o / Np;
     const int n = (int)(o - kl * Np);
     const int64_t d = slot_of[kl];
-    dst[c * total + o] = static_cast<double>(q[c * fstride + ((d >> 5) * Np + n) * 32 + (d & 31)]);
+    dst[c * total + o] =
+        static_cast<double>(q[c * fstride + ((d >> 5) * Np + n) * 32 + ((d & 31) ^ (swm * (n & 3)))]);
   }
 }
 
@@ -364,12 +366,14 @@ void upload_geometry(dg_ctx* c, std::vector<T>& g, std::vector<int32_t>& vp, con
   const dg::Mesh& m = c->mesh;
   g.assign((size_t)c->ntiles * ng * 32, T(0));
   vp.assign((size_t)c->ntiles * NF * 32, 0);
-  // blocked offset of node n of the element in device slot d
-  auto blk = [&](int64_t d, int n) -> int64_t { return ((d >> 5) * Np + n) * 32 + (d & 31); };
+  const int swm = c->km->swizzle;
+  // blocked (column-swizzled) offset of node n of the element in device slot d
+  auto col = [&](int64_t d, int n) -> int64_t { return (d & 31) ^ (swm * (n & 3)); };
+  auto blk = [&](int64_t d, int n) -> int64_t { return ((d >> 5) * Np + n) * 32 + col(d, n); };
   // neighbour node n of the element in slot d2, seen from slot d: same tile -> shared-memory
-  // offset within the tile's field block, encoded negative: -(1 + n*32 + lane2)
+  // offset within the tile's field block, encoded negative: -(1 + n*32 + column)
   auto nbr_code = [&](int64_t d, int64_t d2, int n) -> int64_t {
-    if ((d >> 5) == (d2 >> 5)) return -(1 + (int64_t)n * 32 + (d2 & 31));
+    if ((d >> 5) == (d2 >> 5)) return -(1 + (int64_t)n * 32 + col(d2, n));
     return blk(d2, n);
   };
   for (int64_t d = 0; d < c->Kpad; ++d) {
@@ -511,7 +515,7 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
       const int64_t gd = c->mesh.send_gdof[s];
       const int64_t k = gd / Np, n = gd - (gd / Np) * Np;
       const int64_t d = c->slot_of[c->mesh.g2l[k]];
-      si[s] = (int32_t)(((d >> 5) * Np + n) * 32 + (d & 31));
+      si[s] = (int32_t)(((d >> 5) * Np + n) * 32 + ((d & 31) ^ (c->km->swizzle * (n & 3))));
     }
     if ((st = alloc(c, (void**)&c->send_idx, si.size() * sizeof(int32_t))) != DG_OK) return st;
     CU(c, cudaMemcpy(c->send_idx, si.data(), si.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -659,11 +663,11 @@ dg_status dg_set_fields(dg_ctx* c, const double* Hx, const double* Hy, const dou
     CU(c, cudaMemcpyAsync(c->stage + f * n, src[f], n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   void* q = c->q[c->cur];
   if (c->tsz == 4)
-    to_blocked<float><<<grid_for(3 * c->Kpad * c->ref.Np), 256, 0, c->stream>>>(c->stage, (float*)q, c->perm_d, c->Kl, c->Kpad,
-                                                                               c->ref.Np, c->fstride);
+    to_blocked<float><<<grid_for(3 * c->Kpad * c->ref.Np), 256, 0, c->stream>>>(
+        c->stage, (float*)q, c->perm_d, c->Kl, c->Kpad, c->ref.Np, c->fstride, c->km->swizzle);
   else
-    to_blocked<double><<<grid_for(3 * c->Kpad * c->ref.Np), 256, 0, c->stream>>>(c->stage, (double*)q, c->perm_d, c->Kl,
-                                                                                 c->Kpad, c->ref.Np, c->fstride);
+    to_blocked<double><<<grid_for(3 * c->Kpad * c->ref.Np), 256, 0, c->stream>>>(
+        c->stage, (double*)q, c->perm_d, c->Kl, c->Kpad, c->ref.Np, c->fstride, c->km->swizzle);
   CU(c, cudaGetLastError());
   CU(c, cudaMemsetAsync(c->res, 0, 3 * c->vstride * c->tsz, c->stream));
   c->steps_done = 0;
@@ -678,10 +682,11 @@ dg_status dg_get_fields(dg_ctx* c, double* Hx, double* Hy, double* Ez) {
   const int64_t n = c->Kl * c->ref.Np;
   const void* q = c->q[c->cur];
   if (c->tsz == 4)
-    from_blocked<float><<<grid_for(3 * n), 256, 0, c->stream>>>((const float*)q, c->stage, c->slot_of_d, c->Kl, c->ref.Np, c->fstride);
+    from_blocked<float><<<grid_for(3 * n), 256, 0, c->stream>>>((const float*)q, c->stage, c->slot_of_d, c->Kl,
+                                                                c->ref.Np, c->fstride, c->km->swizzle);
   else
-    from_blocked<double><<<grid_for(3 * n), 256, 0, c->stream>>>((const double*)q, c->stage, c->slot_of_d, c->Kl, c->ref.Np,
-                                                                 c->fstride);
+    from_blocked<double><<<grid_for(3 * n), 256, 0, c->stream>>>((const double*)q, c->stage, c->slot_of_d, c->Kl,
+                                                                 c->ref.Np, c->fstride, c->km->swizzle);
   CU(c, cudaGetLastError());
   double* dst[3] = {Hx, Hy, Ez};
   for (int f = 0; f < 3; ++f)
@@ -804,11 +809,11 @@ dg_status dg_eval_rhs(dg_ctx* c, int32_t which, double* rHx, double* rHy, double
   if ((st = launch_stage(c, mode, a, c->stream, which == 1 ? 1 : 2)) != DG_OK) return st;
   const int64_t n = c->Kl * c->ref.Np;
   if (c->tsz == 4)
-    from_blocked<float><<<grid_for(3 * n), 256, 0, c->stream>>>((const float*)c->out, c->stage, c->slot_of_d, c->Kl, c->ref.Np,
-                                                               c->vstride);
+    from_blocked<float><<<grid_for(3 * n), 256, 0, c->stream>>>((const float*)c->out, c->stage, c->slot_of_d, c->Kl,
+                                                                c->ref.Np, c->vstride, c->km->swizzle);
   else
-    from_blocked<double><<<grid_for(3 * n), 256, 0, c->stream>>>((const double*)c->out, c->stage, c->slot_of_d, c->Kl, c->ref.Np,
-                                                                c->vstride);
+    from_blocked<double><<<grid_for(3 * n), 256, 0, c->stream>>>((const double*)c->out, c->stage, c->slot_of_d, c->Kl,
+                                                                 c->ref.Np, c->vstride, c->km->swizzle);
   CU(c, cudaGetLastError());
   double* dst[3] = {rHx, rHy, rEz};
   for (int f = 0; f < 3; ++f)

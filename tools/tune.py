@@ -20,13 +20,16 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "build_variants")
 
 GRID = {
-    4: [dict(R=r, S=s, C=c) for r, s, c in itertools.product((6, 8, 11), (1, 2), (3, 5))],
-    8: [dict(R=r, S=s, C=c) for r, s, c in itertools.product((4, 6, 8), (1, 2), (3, 5))],
+    4: [dict(R=r, S=s, C=c, M=0) for r, s, c in itertools.product((6, 8, 11), (1, 2), (3, 5))],
+    8: [dict(R=r, S=s, C=c, M=0) for r, s, c in itertools.product((4, 6, 8), (1, 2), (3, 5))]
+    + [dict(R=8, S=s, C=c, M=1) for s, c in itertools.product((1, 2), (2, 3, 4, 6))],
 }
+if os.environ.get("TUNE_GRID") == "mma":  # only the fp64 tensor-core variants
+    GRID = {8: [k for k in GRID[8] if k["M"] == 1]}
 
 
 def name_of(k):
-    return f"R{k['R']}_S{k['S']}_C{k['C']}"
+    return f"R{k['R']}_S{k['S']}_C{k['C']}_M{k['M']}"
 
 
 def cmd_build():
@@ -35,6 +38,8 @@ def cmd_build():
     knobsets = {name_of(k): k for ks in GRID.values() for k in ks}
     for nm, k in sorted(knobsets.items()):
         lib = B.build_variant(nm, k, VDIR)
+        import shutil
+        shutil.rmtree(os.path.join(VDIR, nm), ignore_errors=True)  # keep only the .so (gpurun push size)
         print(lib, flush=True)
 
 
@@ -91,8 +96,13 @@ print(json.dumps(out))
         json.dump(dict(n=n, results=results), fh, indent=1)
 
 
-def cmd_pick(path):
-    d = json.load(open(path))
+def cmd_pick(*paths):
+    d = {"n": None, "results": []}
+    for path in paths:
+        dd = json.load(open(path))
+        d["n"] = dd["n"]
+        d["results"] += dd["results"]
+    path = "+".join(os.path.basename(x) for x in paths)
     best = {}
     chk = {}
     for r in d["results"]:
@@ -107,8 +117,10 @@ def cmd_pick(path):
                     f"{d['n']}x{d['n']} A16 mesh): fastest knob set per (N, precision)"}
     for key, r in sorted(best.items()):
         k = dict(kv.split(":") for kv in [])
-        R, S, C = (int(x[1:]) for x in r["variant"].split("_"))
-        tune[key] = dict(R=R, S=S, C=C, ms=round(r["ms"], 5))
+        parts = r["variant"].split("_")
+        kn = {x[0]: int(x[1:]) for x in parts}
+        kn.setdefault("M", 0)
+        tune[key] = dict(R=kn["R"], S=kn["S"], C=kn["C"], M=kn["M"], ms=round(r["ms"], 5))
     out = os.path.join(ROOT, "paper_1304_5546_b200", "csrc", "tune.json")
     with open(out, "w") as fh:
         json.dump(tune, fh, indent=1)
@@ -121,4 +133,4 @@ if __name__ == "__main__":
     elif sys.argv[1] == "measure":
         cmd_measure(sys.argv[2])
     elif sys.argv[1] == "pick":
-        cmd_pick(sys.argv[2])
+        cmd_pick(*sys.argv[2:])
