@@ -114,25 +114,48 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+CONFIGS = {  # BASELINE.json configs shaped for one bench line (rank-level workloads)
+    "c4": dict(order=5, n=724, prec=4, material=False),   # configs[3]: the north-star target
+    "c5": dict(order=8, n=1448, prec=8, material=True),   # configs[4]: N=8, K=4.19M, fp64, eps 1 | 2.25
+    "c5w": dict(order=8, n=512, prec=8, material=True),   # configs[4] weak scaling: ~524k elements per GPU
+}
+
+
+def initial_fields(x, y, eps=None):
+    """Cavity mode (1,1); with the two-layer material, its exact mode."""
+    if eps is None:
+        return dginputs.cavity_mode(x, y, 0.0)
+    side = np.repeat((np.asarray(eps) > 1.0).astype(int)[:, None], x.shape[1], axis=1)
+    return dginputs.two_layer_mode(x, y, 0.0, side)
+
+
 def workload(args):
     N, n, prec = args.order, args.n, args.prec
     VX, VY, E = dginputs.rect_mesh(n)
     K = E.shape[0]
     Np = (N + 1) * (N + 2) // 2
-    dt = dginputs.cfl_dt(VX, VY, E, N)
-    name = (f"C4-shaped: 2D TM Maxwell PEC unit-square cavity, N={N}, K={K:,} triangles "
-            f"({n}x{n} A16 mesh), {'fp32' if prec == 4 else 'fp64'}, LSERK4, cavity mode (1,1)")
-    return VX, VY, E, K, Np, dt, name
+    eps = mu = None
+    if args.material:
+        eps, mu = dginputs.two_layer_material(VX, VY, E)
+    dt = dginputs.cfl_dt(VX, VY, E, N, eps=eps, mu=mu)
+    tag = {"c4": "C4", "c5": "C5 (strong, 1 rank)", "c5w": "C5 (weak, per-GPU size)"}.get(args.config, "custom")
+    name = (f"{tag}: 2D TM Maxwell PEC unit-square cavity, N={N}, K={K:,} triangles "
+            f"({n}x{n} A16 mesh), {'fp32' if prec == 4 else 'fp64'}, LSERK4, "
+            + ("two-layer eps 1|2.25 material" if args.material else "cavity mode (1,1)"))
+    return VX, VY, E, K, Np, dt, name, eps, mu
 
 
-def oracle_sample(N, n_sample, steps):
+def oracle_sample(N, n_sample, steps, material=False):
     """Time the fp64 NumPy oracle (as it stands) on an n_sample x n_sample mesh."""
     from oracle.solver import Oracle
 
     VX, VY, E = dginputs.rect_mesh(n_sample)
-    o = Oracle(N, VX, VY, E)
-    q = dginputs.cavity_mode(o.geo.x, o.geo.y, 0.0)
-    dt = dginputs.cfl_dt(VX, VY, E, N)
+    eps = mu = None
+    if material:
+        eps, mu = dginputs.two_layer_material(VX, VY, E)
+    o = Oracle(N, VX, VY, E, eps=eps, mu=mu)
+    q = initial_fields(o.geo.x, o.geo.y, eps)
+    dt = dginputs.cfl_dt(VX, VY, E, N, eps=eps, mu=mu)
     t0 = time.perf_counter()
     o.run(q, dt, steps)
     sec = time.perf_counter() - t0
@@ -144,14 +167,17 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     N = args.order
-    _, _, _, K, Np, _, name = workload(args)
+    _, _, _, K, Np, _, name, _, _ = workload(args)
     n_sample = args.ref_n
     from oracle.solver import Oracle
 
     VX, VY, E = dginputs.rect_mesh(n_sample)
-    o = Oracle(N, VX, VY, E)
-    q = dginputs.cavity_mode(o.geo.x, o.geo.y, 0.0)
-    dt = dginputs.cfl_dt(VX, VY, E, N)
+    eps = mu = None
+    if args.material:
+        eps, mu = dginputs.two_layer_material(VX, VY, E)
+    o = Oracle(N, VX, VY, E, eps=eps, mu=mu)
+    q = initial_fields(o.geo.x, o.geo.y, eps)
+    dt = dginputs.cfl_dt(VX, VY, E, N, eps=eps, mu=mu)
     for _ in range(args.warmup):
         q = o.run(q, dt, 1)
     t0 = time.perf_counter()
@@ -159,7 +185,8 @@ def run_reference(args, rank, world):
         q = o.run(q, dt, 1)
     sec = time.perf_counter() - t0
     value = o.Np * o.K * 3 * 5 * args.steps / sec
-    sample = (f"fp64 NumPy oracle, N={N}, {n_sample}x{n_sample} A16 mesh (K={o.K}) per step, "
+    sample = (f"fp64 NumPy oracle, N={N}, {n_sample}x{n_sample} A16 mesh (K={o.K}) per step"
+              f"{', two-layer material' if args.material else ''}, "
               f"{args.steps} steps after {args.warmup} warm-up")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
@@ -185,11 +212,12 @@ def run_ours(args, rank, world, local_rank):
         ids = [dg.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(ids, src=0)
         nccl_id = ids[0]
-    VX, VY, E, K, Np, dt, name = workload(args)
-    ctx = dg.dg_setup(args.order, VX, VY, E, precision=args.prec, device=local_rank, rank=rank,
+    VX, VY, E, K, Np, dt, name, eps, mu = workload(args)
+    ctx = dg.dg_setup(args.order, VX, VY, E, eps=eps, mu=mu, precision=args.prec, device=local_rank, rank=rank,
                       nranks=world, fused=not args.split, transport=0, nccl_id=nccl_id)
     x, y = ctx.nodes()
-    q0 = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in dginputs.cavity_mode(x, y, 0.0)]
+    eps_l = None if eps is None else eps[ctx.local_elements()]
+    q0 = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in initial_fields(x, y, eps_l)]
     ctx.set_fields(*q0)
     stream = torch.cuda.ExternalStream(ctx.stream())
 
@@ -271,15 +299,15 @@ def run_ours(args, rank, world, local_rank):
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, sec, Ks = oracle_sample(args.order, args.ref_n, args.ref_steps)
+        v, sec, Ks = oracle_sample(args.order, args.ref_n, args.ref_steps, args.material)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"fp64 NumPy oracle (single-threaded), N={args.order}, K={Ks} "
                          f"({args.ref_n}x{args.ref_n} mesh), {args.ref_steps} LSERK4 steps, {sec:.1f} s"}
     ws_mb = (2 * 3 * (K // world) * Np * s + 3 * (K // world) * Np * s) / 1e6
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if s == 4 else "f64",
-            "data": "synthetic",
+            "scaling": "weak" if args.config == "c5w" else "strong", "vs_baseline": None,
+            "dtype": "f32" if s == 4 else "f64", "data": "synthetic",
             "config": {"workload": name, "N": args.order, "K": K, "Np": Np, "dt": dt,
                        "variant": "split" if args.split else "fused", "parallelism": f"element-partition x{world}",
                        "l2": f"no flush: per-GPU working set {ws_mb:.0f} MB > 126 MB L2"},
@@ -294,14 +322,24 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--order", type=int, default=5)
-    ap.add_argument("--n", type=int, default=724)
-    ap.add_argument("--prec", type=int, default=4, choices=[4, 8])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + ["custom"],
+                    help="workload preset (BASELINE.json configs); --order/--n/--prec/--material override")
+    ap.add_argument("--order", type=int, default=None)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--prec", type=int, default=None, choices=[4, 8])
+    ap.add_argument("--material", action="store_true", default=None)
     ap.add_argument("--split", action="store_true", help="volume + surface/RK kernels instead of fused")
     ap.add_argument("--ref-n", type=int, default=48, help="oracle sample mesh cells per side")
     ap.add_argument("--ref-steps", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    preset = CONFIGS.get(args.config, CONFIGS["c4"])
+    for key, val in preset.items():
+        if getattr(args, key) is None:
+            setattr(args, key, val)
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config == "c5w" and args.n == CONFIGS["c5w"]["n"]:  # weak scaling: ~524k elements per GPU
+        args.n = {1: 512, 2: 724, 4: 1024, 8: 1448}.get(world_env, int(round(512 * world_env ** 0.5)))
     if args.warmup < 3:
         args.warmup = 3
     world = int(os.environ.get("WORLD_SIZE", "1"))

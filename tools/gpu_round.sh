@@ -1,14 +1,16 @@
 #!/bin/bash
-# One GPU pass for the round's evidence: tests, bench (JSON line), launch list, full ncu of the fused kernel.
+# One GPU pass for the round's evidence: bench lines (C4 fp32/fp64, C5), reference arm,
+# launch list of the default bench, full ncu of the fused kernel (5 stages = 1 LSERK4 step).
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt
 python bench.py --steps 200 --warmup 10 > gpurun_out/bench.json 2> gpurun_out/bench.err
 python bench.py --steps 200 --warmup 10 --prec 8 --no-cpu-baseline > gpurun_out/bench_f64.json 2>> gpurun_out/bench.err
+python bench.py --config c5 --steps 20 --warmup 3 --ref-n 16 --ref-steps 20 > gpurun_out/bench_c5.json 2>> gpurun_out/bench.err
+python bench.py --config c5w --steps 40 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5w.json 2>> gpurun_out/bench.err
 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 8 -c 2 -o gpurun_out/fused_n5_f32 \
-    python tools/prof_one.py 5 4 724 1 2 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 8 -c 2 -o gpurun_out/fused_n5_f64 \
-    python tools/prof_one.py 5 8 724 1 2 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 10 -c 5 -o gpurun_out/fused_n5_f32 \
+    python tools/prof_one.py 5 4 724 1 3 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 10 -c 5 -o gpurun_out/fused_n5_f64 \
+    python tools/prof_one.py 5 8 724 1 3 > /dev/null 2>&1
 ls -la gpurun_out
