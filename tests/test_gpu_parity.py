@@ -9,6 +9,7 @@ checks compare sampled elements against the oracle run on a local patch
 (6+ element rings: a 5-stage step only reaches 5 rings), plus properties.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -256,6 +257,29 @@ def test_c4_full_size_sampled_one_step(c4):
             scale = np.abs(r[F]).max()
             assert np.abs(rhs[F][k] - r[F][loc]).max() <= 1e-5 * 5 * scale
             assert np.abs(got[F][k] - q1[F][loc]).max() <= 2e-5 * max(np.abs(q1[F]).max(), 1e-30)
+
+
+C4_GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "c4_oracle_100steps_sampled.npz")
+
+
+@pytest.mark.skipif(not os.path.exists(C4_GOLDEN), reason="tools/make_c4_golden.py not run")
+def test_c4_full_size_100_steps_vs_oracle(c4):
+    """The bench workload exactly (C4, fp32, fused, 100 steps) against the fp64 oracle run on the
+    WHOLE mesh (tests/golden/c4_oracle_100steps_sampled.npz, written by tools/make_c4_golden.py
+    from oracle/ only), compared on the stored sample of elements: max |error| / max |F_oracle|
+    per field (the A14 metric) <= 2e-5, the north-star fp32 tolerance."""
+    gold = np.load(C4_GOLDEN)
+    c = c4["c"]
+    assert int(gold["N"]) == 5 and int(gold["n"]) == c4["n"] and int(gold["steps"]) == 100
+    dt = float(gold["dt"])
+    assert dt == dginputs.cfl_dt(c4["VX"], c4["VY"], c4["E"], 5)
+    c.set_fields(*c4["q0"])
+    c.run(dt, 100)
+    got = c.get_fields()
+    el = gold["elements"]
+    for F, name in enumerate(("Hx", "Hy", "Ez")):
+        err = np.abs(got[F][el] - gold[name]).max() / float(gold["maxabs"][F])
+        assert err <= 2e-5, (name, err)
 
 
 def test_c4_full_size_100_steps_properties(c4):
