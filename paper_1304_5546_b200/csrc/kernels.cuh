@@ -29,6 +29,7 @@
 //   C  lift:    rhs += LIFT f
 //   D  update:  res = a res + dt rhs;  q_out = q_in + b res
 #include <cstdint>
+#include <cstring>
 #include <type_traits>
 #include <cuda_runtime.h>
 
@@ -62,11 +63,15 @@ constexpr int TL = dg::TILE;
 #define DG_MMA 0  // chosen per (N, precision) by tools/tune.py
 #endif
 constexpr bool USE_MMA = !F32 && DG_MMA;
+// fp32 only: the same contractions as 3xTF32 products on the tensor cores (mma.sync
+// m16n8k8: A = fields, elements x nodes; B = operator^T), split hi + lo so the result
+// keeps fp32 accuracy -- one 16-element m-tile per warp, two warps per tile
+constexpr bool USE_TF = F32 && DG_MMA;
 #ifndef DG_R
 #define DG_R (sizeof(DG_T) == 4 ? 8 : 6)
 #endif
 constexpr int R_TARGET = USE_MMA ? 8 : DG_R;  // max rows per warp
-constexpr int P = (NP + R_TARGET - 1) / R_TARGET;     // warps per tile
+constexpr int P = USE_TF ? 2 : (NP + R_TARGET - 1) / R_TARGET;  // warps per tile
 constexpr int R = (NP + P - 1) / P;                // rows per warp
 constexpr int RP = P * R;                          // padded rows (extra rows are zero)
 constexpr int TEAM = P * 32;
@@ -75,7 +80,8 @@ constexpr int TEAM = P * 32;
 constexpr int VC = F32 ? 2 : 1;
 constexpr int NPC = (NP + VC - 1) / VC;  // Dr/Ds column groups
 constexpr int NFC = (NF + VC - 1) / VC;  // LIFT column groups
-constexpr int NFE = NFC * VC;            // padded face points per element (flux buffer width)
+// padded face points per element (flux buffer width; TF32: whole k-steps of 8, pad rows zero)
+constexpr int NFE = USE_TF ? 8 * ((NF + 7) / 8) : NFC * VC;
 
 // shared-memory layout (bytes; each piece a multiple of 16 B)
 //   ops : DV[NPC][RP] (fp32 float4 {Dr_j, Ds_j, Dr_j+1, Ds_j+1} | fp64 double2 {Dr_j, Ds_j})
@@ -86,14 +92,23 @@ constexpr int NFE = NFC * VC;            // padded face points per element (flux
 //         holding its m8n8k4 A-fragment element (row 8g + lane/4, column 4k + lane%4)
 constexpr int KV = (NP + 3) / 4;  // MMA k-steps of the volume contraction
 constexpr int KL = (NF + 3) / 4;  // MMA k-steps of the LIFT contraction
-constexpr size_t DVB = USE_MMA ? (size_t)KV * P * 32 * 16 : (size_t)NPC * RP * 2 * VC * sizeof(T);
+//   TF32 ops (fp32): BV[KVT][NT][hi, lo][32] float4 {Dr b0, Dr b1, Ds b0, Ds b1} and
+//         BL[KLT][NT][32] float4 {hi b0, hi b1, lo b0, lo b1}, each lane holding its
+//         m16n8k8 B-fragment elements (k = 8ks + lane%4 (+4), n = 8nt + lane/4)
+constexpr int NT = (NP + 7) / 8;   // TF32 n-tiles (8 output rows each)
+constexpr int KVT = (NP + 7) / 8;  // TF32 k-steps of the volume contraction
+constexpr int KLT = (NF + 7) / 8;  // TF32 k-steps of the LIFT contraction
 constexpr int RPL = (RP + 1) & ~1;  // LIFT rows padded to even
-constexpr size_t LVB = USE_MMA ? (size_t)KL * P * 32 * 8 : (size_t)NFC * RPL * VC * sizeof(T);
+constexpr size_t DVB = USE_TF ? (size_t)KVT * NT * 32 * 32
+                              : USE_MMA ? (size_t)KV * P * 32 * 16 : (size_t)NPC * RP * 2 * VC * sizeof(T);
+constexpr size_t LVB = USE_TF ? (size_t)KLT * NT * 32 * 16
+                              : USE_MMA ? (size_t)KL * P * 32 * 8 : (size_t)NFC * RPL * VC * sizeof(T);
 constexpr size_t OPB = ((DVB + LVB + 15) / 16) * 16;
 // Column swizzle of the tile-blocked layout: element e of node row n is stored at
 // column e ^ (SWM * (n & 3)).  Identity for the FMA kernels; for the DMMA kernels
-// it makes the B-fragment loads (4 rows x 8 elements) bank-conflict free.
-constexpr int SWM = USE_MMA ? 4 : 0;
+// it makes the B-fragment loads (4 rows x 8 elements) bank-conflict free, for the
+// TF32 kernels the A-fragment loads (8 elements x 4 nodes).
+constexpr int SWM = USE_MMA ? 4 : (USE_TF ? 8 : 0);
 __host__ __device__ constexpr int colx(int n, int e) { return e ^ (SWM * (n & 3)); }
 constexpr size_t QB = (size_t)3 * NP * TL * sizeof(T);
 __host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)(mat ? dg::NGEO_MAT : dg::NGEO_CONST) * TL * sizeof(T); }
@@ -299,6 +314,7 @@ __device__ __forceinline__ void volume_mma(const double* __restrict__ sq, const 
     syb[nt] = sg[3 * TL + eb];
     u[nt][0] = u[nt][1] = v[nt][0] = v[nt][1] = w[nt][0] = w[nt][1] = 0.0;
   }
+  double w2acc[4][2] = {};  // Ds W2 in its own accumulator: 4 independent DMMA chains per n-tile
 #pragma unroll
   for (int ks = 0; ks < KV; ++ks) {
     const int j = 4 * ks + (lane & 3);
@@ -313,8 +329,13 @@ __device__ __forceinline__ void volume_mma(const double* __restrict__ sq, const 
       dmma(u[nt][0], u[nt][1], a.x, ez);
       dmma(v[nt][0], v[nt][1], a.y, ez);
       dmma(w[nt][0], w[nt][1], a.x, w1);
-      dmma(w[nt][0], w[nt][1], a.y, w2);
+      dmma(w2acc[nt][0], w2acc[nt][1], a.y, w2);
     }
+  }
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    w[nt][0] += w2acc[nt][0];
+    w[nt][1] += w2acc[nt][1];
   }
 }
 
@@ -334,6 +355,195 @@ __device__ __forceinline__ void lift_mma(const double* __restrict__ sp, const do
       dmma(rez[nt][0], rez[nt][1], a, sp[2 * NFE * TL + addr]);
     }
   }
+}
+
+// ---------------------------------------------------------------- 3xTF32 (fp32 tensor core) path
+// D(16x8) += A(16x8) B(8x8), tf32 operands, fp32 accumulation.  Lane (grp = lane/4,
+// tig = lane%4) holds A[grp][tig], A[grp+8][tig], A[grp][tig+4], A[grp+8][tig+4];
+// B[tig][grp], B[tig+4][grp]; C[grp][2tig + {0,1}], C[grp+8][2tig + {0,1}].
+__device__ __forceinline__ void tmma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// x = hi + lo: hi = x rounded to nearest (ties away) at tf32's 10 mantissa bits by integer
+// add + mask -- the same rounding as cvt.rna.tf32 for finite x, without its NaN/Inf
+// handling (4 more instructions) -- and lo = x - hi, exact in fp32, read by the MMA as tf32
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
+}
+// c += A B with A = ah + al, B = bh + bl; the al bl term (~2^-22 relative) is dropped
+__device__ __forceinline__ void tmma3(float (&c)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], float bh0,
+                                      float bh1, float bl0, float bl1) {
+  tmma(c, al, __float_as_uint(bh0), __float_as_uint(bh1));
+  tmma(c, ah, __float_as_uint(bl0), __float_as_uint(bl1));
+  tmma(c, ah, __float_as_uint(bh0), __float_as_uint(bh1));
+}
+
+// One tile on the 3xTF32 path (fp32): elements are the MMA rows -- warp g owns
+// elements e = 16g + lane/4 (+8) -- and each n-tile is 8 output rows, so the padding is
+// only Np -> 8 NT.  Volume (u = Dr Ez, v = Ds Ez, w = Dr W1 + Ds W2, as volume_rows)
+// -> flux (flux_points, one lane per element) -> LIFT -> material scaling -> LSERK4.
+// C-fragment register r of n-tile nt is element ee[r >> 1], row 8nt + 2(lane%4) + (r & 1).
+template <int MODE, bool MAT, typename TT>
+__device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
+                                        TT* __restrict__ sp, const unsigned char* __restrict__ ops,
+                                        const int32_t (&vmc)[KPT], int tile, int g, int lane, TT alpha,
+                                        bool read_res) {
+  using MT = ModeTraits<MODE>;
+  const int tig = lane & 3;
+  const int ee[2] = {16 * g + (lane >> 2), 16 * g + (lane >> 2) + 8};
+  // Lane-invariant shared-memory offsets.  A fragments read node rows 8ks + 4kh + tig, whose
+  // swizzle (row & 3 = tig) does not depend on (ks, kh): row offsets are compile-time.  Rows
+  // past Np / 3Nfp meet zero B rows; they read the next field, the geometry block (fields) or
+  // zeroed pad rows (flux), all finite.  C fragments: row 8nt + 2tig + h, element ee[i].
+  const int abase[2] = {tig * TL + (ee[0] ^ (8 * tig)), tig * TL + (ee[1] ^ (8 * tig))};
+  int cbase[4];  // C register r -> row (2tig + (r & 1)) offset + swizzled column of ee[r >> 1]
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int n = 2 * tig + (r & 1);
+    cbase[r] = n * TL + colx(n, ee[r >> 1]);
+  }
+  auto row_ok = [&](int nt, int r) { return NT * 8 == NP || nt < NT - 1 || 8 * nt + 2 * tig + (r & 1) < NP; };
+  const int64_t tbase = (int64_t)tile * NP * TL;
+  TT acc[3][NT][4];
+  if constexpr (MT::vol) {
+    TT rxe[2], sxe[2], rye[2], sye[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      rxe[i] = sg[0 * TL + ee[i]];
+      sxe[i] = sg[1 * TL + ee[i]];
+      rye[i] = sg[2 * TL + ee[i]];
+      sye[i] = sg[3 * TL + ee[i]];
+    }
+    TT u[NT][4], v[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) u[nt][r] = v[nt][r] = acc[2][nt][r] = TT(0);
+    const float4* BV = reinterpret_cast<const float4*>(ops) + lane;
+#pragma unroll
+    for (int ks = 0; ks < KVT; ++ks) {
+      uint32_t ezh[4], ezl[4], w1h[4], w1l[4], w2h[4], w2l[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {  // A register r: element ee[r & 1], node 8ks + tig + 4(r >> 1)
+        const int i = r & 1;
+        const TT* a = sq + abase[i] + (8 * ks + 4 * (r >> 1)) * TL;
+        const TT hx = a[0], hy = a[NP * TL], ez = a[2 * NP * TL];
+        split_tf32(ez, ezh[r], ezl[r]);
+        split_tf32(rxe[i] * hy - rye[i] * hx, w1h[r], w1l[r]);
+        split_tf32(sxe[i] * hy - sye[i] * hx, w2h[r], w2l[r]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const float4 bh = BV[(ks * NT + nt) * 64];  // hi and lo: 32 lanes x 16 B contiguous each
+        const float4 bl = BV[(ks * NT + nt) * 64 + 32];
+        tmma3(u[nt], ezh, ezl, bh.x, bh.y, bl.x, bl.y);
+        tmma3(v[nt], ezh, ezl, bh.z, bh.w, bl.z, bl.w);
+        tmma3(acc[2][nt], w1h, w1l, bh.x, bh.y, bl.x, bl.y);
+        tmma3(acc[2][nt], w2h, w2l, bh.z, bh.w, bl.z, bl.w);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = r >> 1;
+        acc[0][nt][r] = -(rye[i] * u[nt][r] + sye[i] * v[nt][r]);
+        acc[1][nt][r] = rxe[i] * u[nt][r] + sxe[i] * v[nt][r];
+      }
+  } else if constexpr (MODE == dg::MODE_SURFACE_RK) {
+    const TT* __restrict__ rv = static_cast<const TT*>(p.rhsv) + tbase;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          acc[c][nt][r] = row_ok(nt, r) ? rv[c * p.vstride + 8 * nt * TL + cbase[r]] : TT(0);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[c][nt][r] = TT(0);
+  }
+  // LSERK4 residual -> registers (in flight during the surface phase)
+  TT rr[3][NT][4];
+  if constexpr (MT::rk) {
+    if (read_res) {
+      const TT* __restrict__ res = static_cast<const TT*>(p.res) + tbase;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            rr[c][nt][r] = row_ok(nt, r) ? __ldcs(res + c * p.vstride + 8 * nt * TL + cbase[r]) : TT(0);
+    }
+  }
+  if constexpr (MT::surf) {
+    flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
+    __syncthreads();
+    const float4* BL = reinterpret_cast<const float4*>(ops + DVB) + lane;
+#pragma unroll
+    for (int ks = 0; ks < KLT; ++ks) {
+      uint32_t fh[3][4], fl[3][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const TT* a = sp + abase[r & 1] + (8 * ks + 4 * (r >> 1)) * TL;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) split_tf32(a[c * NFE * TL], fh[c][r], fl[c][r]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const float4 b = BL[(ks * NT + nt) * 32];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) tmma3(acc[c][nt], fh[c], fl[c], b.x, b.y, b.z, b.w);
+      }
+    }
+  }
+  if constexpr (MAT) {
+    if (MODE != dg::MODE_VOLUME || p.scale_volume) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const TT imu = sg[16 * TL + ee[i]], ieps = sg[17 * TL + ee[i]];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            acc[0][nt][2 * i + h] *= imu;
+            acc[1][nt][2 * i + h] *= imu;
+            acc[2][nt][2 * i + h] *= ieps;
+          }
+      }
+    }
+  }
+  const TT a = static_cast<TT>(p.a), b = static_cast<TT>(p.b), dt = static_cast<TT>(p.dt);
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (!row_ok(nt, r)) continue;
+      const int o = 8 * nt * TL + cbase[r];
+      if constexpr (MT::rk) {
+        TT* __restrict__ res = static_cast<TT*>(p.res) + tbase;
+        TT* __restrict__ qo = static_cast<TT*>(p.q_out) + tbase;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          TT rs = dt * acc[c][nt][r];
+          if (read_res) rs = fma(a, rr[c][nt][r], rs);
+          if (p.write_res) __stcs(res + c * p.vstride + o, rs);
+          __stcs(qo + c * p.fstride + o, fma(b, rs, sq[c * NP * TL + o]));
+        }
+      } else {
+        TT* __restrict__ out = static_cast<TT*>(p.out) + tbase;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) out[c * p.vstride + o] = acc[c][nt][r];
+      }
+    }
 }
 
 // ---------------------------------------------------------------- phase C: lift
@@ -611,6 +821,8 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     T* sp = sp_of(s);
     if constexpr (USE_MMA) {
       mma_tile<MODE, MAT>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, lane, alpha, read_res);
+    } else if constexpr (USE_TF) {
+      tf_tile<MODE, MAT>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, lane, alpha, read_res);
     } else {
     T rhx[R], rhy[R], rez[R];
     if constexpr (MT::vol) {
@@ -769,6 +981,43 @@ void pack_ops(const double* Dr, const double* Ds, const double* LIFT, void* out)
           const int m = 4 * ks + ln % 4;
           if (n < NP && m < NF) al[(size_t)(ks * P + g) * 32 + ln] = static_cast<T>(LIFT[n * NF + m]);
         }
+      }
+    return;
+  }
+  if constexpr (USE_TF) {  // B fragments: lane -> (k = 8ks + lane%4 (+4), output row 8nt + lane/4)
+    auto tf32_hi = [](double x) {  // round to nearest (ties away) at 10 mantissa bits, as cvt.rna.tf32
+      const float f = static_cast<float>(x);
+      uint32_t u;
+      std::memcpy(&u, &f, 4);
+      u = (u + 0x1000u) & 0xFFFFE000u;
+      float h;
+      std::memcpy(&h, &u, 4);
+      return h;
+    };
+    float* bv = reinterpret_cast<float*>(o);
+    float* bl = reinterpret_cast<float*>(o + DVB);
+    for (int nt = 0; nt < NT; ++nt)
+      for (int ln = 0; ln < 32; ++ln) {
+        const int n = 8 * nt + ln / 4;
+        for (int ks = 0; ks < KVT; ++ks)
+          for (int kh = 0; kh < 2; ++kh) {
+            const int j = 8 * ks + ln % 4 + 4 * kh;
+            const double dr = (n < NP && j < NP) ? Dr[n * NP + j] : 0.0;
+            const double ds = (n < NP && j < NP) ? Ds[n * NP + j] : 0.0;
+            float* e = bv + ((size_t)(ks * NT + nt) * 64 + ln) * 4;  // float4 hi; float4 lo 32 lanes on
+            e[0 + kh] = tf32_hi(dr);
+            e[2 + kh] = tf32_hi(ds);
+            e[128 + kh] = tf32_hi(dr - tf32_hi(dr));  // lo parts rounded to tf32 here (free), not
+            e[130 + kh] = tf32_hi(ds - tf32_hi(ds));  // truncated by the MMA
+          }
+        for (int ks = 0; ks < KLT; ++ks)
+          for (int kh = 0; kh < 2; ++kh) {
+            const int m = 8 * ks + ln % 4 + 4 * kh;
+            const double l = (n < NP && m < NF) ? LIFT[n * NF + m] : 0.0;
+            float* e = bl + ((size_t)(ks * NT + nt) * 32 + ln) * 4;
+            e[kh] = tf32_hi(l);
+            e[2 + kh] = tf32_hi(l - tf32_hi(l));
+          }
       }
     return;
   }

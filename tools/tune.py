@@ -3,7 +3,8 @@
 
     python tools/tune.py build            # CPU: build one library per knob set -> build_variants/
     python tools/tune.py measure OUT.json # GPU: time the fused stage for every (variant, N, precision)
-    python tools/tune.py pick OUT.json    # CPU: write paper_1304_5546_b200/csrc/tune.json
+    python tools/tune.py pick OUT.json... # CPU: write paper_1304_5546_b200/csrc/tune.json
+                                          #   (OUT.json:f64 = only that file's fp64 rows)
 
 Knobs: R (max rows per warp -> team size), S (shared-memory slots), C (teams/SM cap).
 Timing: one LSERK4 stage = one fused launch, CUDA events, mean of 5 steps after warm-up,
@@ -26,6 +27,8 @@ GRID = {
 }
 if os.environ.get("TUNE_GRID") == "mma":  # only the fp64 tensor-core variants
     GRID = {8: [k for k in GRID[8] if k["M"] == 1]}
+if os.environ.get("TUNE_GRID") == "tf":  # tensor-core variants (fp32 3xTF32, fp64 DMMA)
+    GRID = {4: [dict(R=8, S=s, C=c, M=1) for s, c in itertools.product((1, 2), (3, 4, 6, 8, 12))]}
 
 
 def name_of(k):
@@ -98,11 +101,12 @@ print(json.dumps(out))
 
 def cmd_pick(*paths):
     d = {"n": None, "results": []}
-    for path in paths:
+    for arg in paths:  # PATH or PATH:f32 / PATH:f64 (take only that precision's rows)
+        path, _, only = arg.partition(":")
         dd = json.load(open(path))
         d["n"] = dd["n"]
-        d["results"] += dd["results"]
-    path = "+".join(os.path.basename(x) for x in paths)
+        d["results"] += [r for r in dd["results"] if not only or only == ("f32" if r["prec"] == 4 else "f64")]
+    path = "+".join(os.path.basename(x) for x in paths)  # noqa: keeps the :prec selectors
     best = {}
     chk = {}
     for r in d["results"]:
@@ -114,7 +118,8 @@ def cmd_pick(*paths):
         if key not in best or r["ms"] < best[key]["ms"]:
             best[key] = r
     tune = {"_doc": f"picked by tools/tune.py from {os.path.basename(path)} (fused stage, "
-                    f"{d['n']}x{d['n']} A16 mesh): fastest knob set per (N, precision)"}
+                    f"{d['n']}x{d['n']} A16 mesh): fastest knob set per (N, precision); M=1: tensor-core "
+                    f"path (fp32 3xTF32 mma.sync, fp64 DMMA)"}
     for key, r in sorted(best.items()):
         k = dict(kv.split(":") for kv in [])
         parts = r["variant"].split("_")
