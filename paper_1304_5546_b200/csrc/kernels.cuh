@@ -113,9 +113,19 @@ __host__ __device__ constexpr int colx(int n, int e) { return e ^ (SWM * (n & 3)
 constexpr size_t QB = (size_t)3 * NP * TL * sizeof(T);
 __host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)(mat ? dg::NGEO_MAT : dg::NGEO_CONST) * TL * sizeof(T); }
 constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
-__host__ __device__ constexpr size_t slot_bytes(bool surf, bool mat) { return QB + geo_bytes(mat) + (surf ? SPB : 0); }
+// DG_RT (TF32 path only): the LSERK4 residual of the slot's tile also arrives by TMA into
+// shared memory (frees ~12 NT registers per thread) instead of a register prefetch.
+#ifndef DG_RT
+#define DG_RT 1
+#endif
+constexpr bool RES_TMA = USE_TF && DG_RT;
+__host__ __device__ constexpr size_t slot_bytes(bool surf, bool mat, bool rk) {
+  return QB + geo_bytes(mat) + (surf ? SPB : 0) + (RES_TMA && rk ? QB : 0);
+}
 constexpr size_t BARB = 64;  // mbarriers: one per slot
-__host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat) { return BARB + OPB + S * slot_bytes(surf, mat); }
+__host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat, bool rk) {
+  return BARB + OPB + S * slot_bytes(surf, mat, rk);
+}
 // Slots per team: 2 = double-buffered (tile t+1 streams in while t computes), 1 = latency
 // hidden across resident teams instead.  Measured at C4 (N=5): fp32 is issue-bound and
 // prefers more resident teams (1 slot), fp64 is latency-bound and prefers 2 slots.
@@ -123,7 +133,7 @@ __host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat) { re
 #define DG_S (sizeof(DG_T) == 4 ? 1 : 2)
 #endif
 __host__ __device__ constexpr int nslots(bool, bool) { return DG_S; }
-constexpr int CTAS_BY_SMEM = (int)((227 * 1024) / smem_total(nslots(true, false), true, false));
+constexpr int CTAS_BY_SMEM = (int)((227 * 1024) / smem_total(nslots(true, false), true, false, true));
 #ifndef DG_C
 #define DG_C 5  // measured (C4 fp32): 5 teams x 128 registers beats 8 x 80 (spills) and 4 x 168
 #endif
@@ -388,9 +398,9 @@ __device__ __forceinline__ void tmma3(float (&c)[4], const uint32_t (&ah)[4], co
 // C-fragment register r of n-tile nt is element ee[r >> 1], row 8nt + 2(lane%4) + (r & 1).
 template <int MODE, bool MAT, typename TT>
 __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
-                                        TT* __restrict__ sp, const unsigned char* __restrict__ ops,
-                                        const int32_t (&vmc)[KPT], int tile, int g, int lane, TT alpha,
-                                        bool read_res) {
+                                        TT* __restrict__ sp, const TT* __restrict__ sr,
+                                        const unsigned char* __restrict__ ops, const int32_t (&vmc)[KPT],
+                                        int tile, int g, int lane, TT alpha, bool read_res) {
   using MT = ModeTraits<MODE>;
   const int tig = lane & 3;
   const int ee[2] = {16 * g + (lane >> 2), 16 * g + (lane >> 2) + 8};
@@ -470,9 +480,9 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
 #pragma unroll
         for (int r = 0; r < 4; ++r) acc[c][nt][r] = TT(0);
   }
-  // LSERK4 residual -> registers (in flight during the surface phase)
+  // LSERK4 residual -> registers (DG_RT=0; in flight during the surface phase)
   TT rr[3][NT][4];
-  if constexpr (MT::rk) {
+  if constexpr (MT::rk && !RES_TMA) {
     if (read_res) {
       const TT* __restrict__ res = static_cast<const TT*>(p.res) + tbase;
 #pragma unroll
@@ -534,7 +544,7 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           TT rs = dt * acc[c][nt][r];
-          if (read_res) rs = fma(a, rr[c][nt][r], rs);
+          if (read_res) rs = fma(a, RES_TMA ? sr[c * NP * TL + o] : rr[c][nt][r], rs);
           if (p.write_res) __stcs(res + c * p.vstride + o, rs);
           __stcs(qo + c * p.fstride + o, fma(b, rs, sq[c * NP * TL + o]));
         }
@@ -705,7 +715,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   using MT = ModeTraits<MODE>;
   constexpr int NG = MAT ? dg::NGEO_MAT : dg::NGEO_CONST;
   constexpr int S = nslots(MT::surf, MAT);
-  constexpr size_t SLOT = slot_bytes(MT::surf, MAT);
+  constexpr size_t SLOT = slot_bytes(MT::surf, MAT, MT::rk);
   constexpr size_t GB = geo_bytes(MAT);
   constexpr int CH = 16 / (int)sizeof(T);
   constexpr int QC = NP * TL / CH;  // 16 B chunks per field tile
@@ -724,6 +734,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   auto sq_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT); };
   auto sg_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB); };
   auto sp_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB + GB); };
+  auto sr_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB + GB + (MT::surf ? SPB : 0)); };
   const bool read_res = MT::rk && p.a != 0.0;
   const int g = tid >> 5, lane = tid & 31;
 
@@ -748,12 +759,19 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       const int tile = tile_of(it);
       const int s = it % S;
       uint64_t* bar = bars + s;
-      mbar_expect_tx(bar, (unsigned)(QB + GB));
+      constexpr bool rt = RES_TMA && MT::rk;
+      mbar_expect_tx(bar, (unsigned)(QB + GB + (rt && read_res ? QB : 0)));
       T* sq = sq_of(s);
 #pragma unroll
       for (int c = 0; c < 3; ++c)
         tma_load_1d(sq + c * NP * TL, q + c * p.fstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bar);
       tma_load_1d(sg_of(s), geo + (int64_t)tile * NG * TL, (unsigned)GB, bar);
+      if (rt && read_res) {
+        const T* res = static_cast<const T*>(p.res);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          tma_load_1d(sr_of(s) + c * NP * TL, res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bar);
+      }
     }
   };
   // cross-tile neighbour traces of tile `it` (same-tile ones are read from shared memory)
@@ -822,7 +840,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     if constexpr (USE_MMA) {
       mma_tile<MODE, MAT>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, lane, alpha, read_res);
     } else if constexpr (USE_TF) {
-      tf_tile<MODE, MAT>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, lane, alpha, read_res);
+      tf_tile<MODE, MAT>(p, sq, sg_of(s), sp, sr_of(s), smem_raw + BARB, vc0, tile, g, lane, alpha, read_res);
     } else {
     T rhx[R], rhy[R], rez[R];
     if constexpr (MT::vol) {
@@ -913,7 +931,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
 template <int MODE, bool MAT>
 cudaError_t launch_one(const dg::StageArgs& a, cudaStream_t s) {
   using MT = ModeTraits<MODE>;
-  constexpr size_t smem = smem_total(nslots(MT::surf, MAT), MT::surf, MAT);
+  constexpr size_t smem = smem_total(nslots(MT::surf, MAT), MT::surf, MAT, MT::rk);
   static int grid_cap[64] = {0};  // resident CTAs (whole GPU) per device ordinal
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -1057,7 +1075,7 @@ dg::KernelInfo info() {
   k.slots = nslots(true, false);
   k.row_groups = P;
   k.rows_per_group = R;
-  k.smem_bytes = smem_total(nslots(true, false), true, false);
+  k.smem_bytes = smem_total(nslots(true, false), true, false, true);
   return k;
 }
 

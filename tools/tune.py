@@ -28,11 +28,11 @@ GRID = {
 if os.environ.get("TUNE_GRID") == "mma":  # only the fp64 tensor-core variants
     GRID = {8: [k for k in GRID[8] if k["M"] == 1]}
 if os.environ.get("TUNE_GRID") == "tf":  # tensor-core variants (fp32 3xTF32, fp64 DMMA)
-    GRID = {4: [dict(R=8, S=s, C=c, M=1) for s, c in itertools.product((1, 2), (3, 4, 6, 8, 12))]}
+    GRID = {4: [dict(R=8, S=s, C=c, M=1, Q=q) for s, c, q in itertools.product((1, 2), (3, 4, 6), (0, 1))]}
 
 
 def name_of(k):
-    return f"R{k['R']}_S{k['S']}_C{k['C']}_M{k['M']}"
+    return f"R{k['R']}_S{k['S']}_C{k['C']}_M{k['M']}" + (f"_Q{k['Q']}" if "Q" in k else "")
 
 
 def cmd_build():
@@ -125,7 +125,8 @@ def cmd_pick(*paths):
         parts = r["variant"].split("_")
         kn = {x[0]: int(x[1:]) for x in parts}
         kn.setdefault("M", 0)
-        tune[key] = dict(R=kn["R"], S=kn["S"], C=kn["C"], M=kn["M"], ms=round(r["ms"], 5))
+        kn.setdefault("Q", 0)  # sweeps before the knob existed: register prefetch
+        tune[key] = dict(R=kn["R"], S=kn["S"], C=kn["C"], M=kn["M"], Q=kn["Q"], ms=round(r["ms"], 5))
     out = os.path.join(ROOT, "paper_1304_5546_b200", "csrc", "tune.json")
     with open(out, "w") as fh:
         json.dump(tune, fh, indent=1)
