@@ -247,6 +247,7 @@ def run_ours(args, rank, world, local_rank):
         barrier()
     ms = e0.elapsed_time(e1)
     stats = ctx.kernel_stats()
+    kcfg = ctx.kernel_config()
     ctx.profile(False)
     ctx.sync()
     if dist is not None:
@@ -310,7 +311,11 @@ def run_ours(args, rank, world, local_rank):
             "dtype": "f32" if s == 4 else "f64", "data": "synthetic",
             "config": {"workload": name, "N": args.order, "K": K, "Np": Np, "dt": dt,
                        "variant": "split" if args.split else "fused", "parallelism": f"element-partition x{world}",
-                       "l2": f"no flush: per-GPU working set {ws_mb:.0f} MB > 126 MB L2"},
+                       "l2": f"no flush: per-GPU working set {ws_mb:.0f} MB > 126 MB L2",
+                       "contraction": {"fma": "CUDA-core FMA", "dmma_fp64": "fp64 tensor cores (DMMA)",
+                                       "3xtf32": "fp32 via 3xTF32 tensor-core split (hi*hi+lo*hi+hi*lo, "
+                                                 "fp32 accumulate)"}[kcfg["contraction"]],
+                       "kernel_config": kcfg},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "wall_s_timed": t_wall}
     print(json.dumps(line), flush=True)

@@ -184,6 +184,22 @@ dg_status dg_profile(dg_ctx* c, int32_t enable);
 /* Read the statistics (synchronises the stream when profiling is on). */
 dg_status dg_get_kernel_stats(dg_ctx* c, dg_kernel_stats* out);
 
+/* The stage-kernel configuration compiled for this context's (N, precision): the knob set
+ * tools/tune.py picked (csrc/tune.json).  Host-only contexts included. */
+typedef struct {
+  int32_t contraction;   /* volume + LIFT contractions: 0 = CUDA-core FMA (FFMA/DFMA),
+                            1 = fp64 tensor cores (DMMA, mma.sync m8n8k4),
+                            2 = fp32 on tensor cores as 3xTF32 (mma.sync m16n8k8; each operand
+                                split hi + lo, hi*hi + lo*hi + hi*lo in fp32 accumulation) */
+  int32_t threads;       /* threads per CTA; one CTA owns one 32-element tile at a time */
+  int32_t slots;         /* shared-memory pipeline slots (1 or 2) */
+  int32_t residual_tma;  /* 1: the LSERK4 residual is staged into shared memory by TMA */
+  int32_t teams_cap;     /* cap on resident CTAs per SM (launch bounds) */
+  int32_t reserved;
+  int64_t smem_bytes;    /* dynamic shared memory per CTA of the fused stage kernel */
+} dg_kernel_config;
+dg_status dg_get_kernel_config(const dg_ctx* c, dg_kernel_config* out);
+
 /* Release everything.  Accepts NULL. */
 void dg_destroy(dg_ctx* c);
 

@@ -57,6 +57,9 @@ struct KernelInfo {
   int N, prec;                       // prec = 4 or 8
   int threads, slots, row_groups, rows_per_group;
   size_t smem_bytes;
+  int contraction;   // 0 FMA, 1 fp64 DMMA, 2 fp32 3xTF32 (dg.h dg_kernel_config)
+  int residual_tma;  // LSERK4 residual staged by TMA
+  int teams_cap;     // DG_C
 };
 
 struct KernelModule {

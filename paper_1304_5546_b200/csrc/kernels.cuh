@@ -1076,6 +1076,9 @@ dg::KernelInfo info() {
   k.row_groups = P;
   k.rows_per_group = R;
   k.smem_bytes = smem_total(nslots(true, false), true, false, true);
+  k.contraction = USE_TF ? 2 : (USE_MMA ? 1 : 0);
+  k.residual_tma = RES_TMA ? 1 : 0;
+  k.teams_cap = DG_C;
   return k;
 }
 

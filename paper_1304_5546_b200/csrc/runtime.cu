@@ -957,6 +957,23 @@ dg_status dg_get_kernel_stats(dg_ctx* c, dg_kernel_stats* out) {
   return DG_OK;
 }
 
+dg_status dg_get_kernel_config(const dg_ctx* c, dg_kernel_config* out) {
+  dg_status st = check_usable(c, false);
+  if (st != DG_OK) return st;
+  if (!out) return set_err(DG_E_ARG, "null output");
+  const dg::KernelModule* km = c->km ? c->km : dg::find_module(c->N, c->prec);  // host-only: lookup
+  if (!km) return set_err(DG_E_DEGREE, "no kernel module compiled for N=" + std::to_string(c->N));
+  const dg::KernelInfo k = km->info();
+  out->contraction = k.contraction;
+  out->threads = k.threads;
+  out->slots = k.slots;
+  out->residual_tma = k.residual_tma;
+  out->teams_cap = k.teams_cap;
+  out->reserved = 0;
+  out->smem_bytes = (int64_t)k.smem_bytes;
+  return DG_OK;
+}
+
 void dg_destroy(dg_ctx* c) {
   if (!c) return;
   if (!c->host_only) {

@@ -32,8 +32,8 @@ STATUS = {0: "DG_OK", 1: "DG_E_ARG", 2: "DG_E_DEGREE", 3: "DG_E_MESH_DEGENERATE"
 EXPORTS = ["dg_options_default", "dg_setup", "dg_sizes", "dg_local_elements", "dg_set_fields",
            "dg_get_fields", "dg_run", "dg_run_group", "dg_sync", "dg_eval_rhs", "dg_energy",
            "dg_get_operators", "dg_get_geometry", "dg_get_maps", "dg_get_nodes", "dg_halo_sizes",
-           "dg_get_halo", "dg_stream", "dg_profile", "dg_get_kernel_stats", "dg_destroy",
-           "dg_last_error"]
+           "dg_get_halo", "dg_stream", "dg_profile", "dg_get_kernel_stats", "dg_get_kernel_config",
+           "dg_destroy", "dg_last_error"]
 
 
 class DGError(RuntimeError):
@@ -55,6 +55,15 @@ class KernelStats(C.Structure):
 
 
 KIND = ("fused", "volume", "surface", "helper")
+
+
+class KernelConfig(C.Structure):
+    _fields_ = [("contraction", C.c_int32), ("threads", C.c_int32), ("slots", C.c_int32),
+                ("residual_tma", C.c_int32), ("teams_cap", C.c_int32), ("reserved", C.c_int32),
+                ("smem_bytes", C.c_int64)]
+
+
+CONTRACTION = ("fma", "dmma_fp64", "3xtf32")
 
 _vp = C.c_void_p
 _i64 = C.c_int64
@@ -80,6 +89,7 @@ _sig = {
     "dg_stream": [_vp, _P(_vp)],
     "dg_profile": [_vp, C.c_int32],
     "dg_get_kernel_stats": [_vp, _vp],
+    "dg_get_kernel_config": [_vp, _vp],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -258,6 +268,13 @@ class Context:
 
     def profile(self, enable=True):
         _check(_lib.dg_profile(self._h, 1 if enable else 0))
+
+    def kernel_config(self):
+        """dg_get_kernel_config: the compiled stage-kernel configuration of this (N, precision)."""
+        k = KernelConfig()
+        _check(_lib.dg_get_kernel_config(self._h, C.byref(k)))
+        return dict(contraction=CONTRACTION[k.contraction], threads=k.threads, slots=k.slots,
+                    residual_tma=bool(k.residual_tma), teams_cap=k.teams_cap, smem_bytes=k.smem_bytes)
 
     def kernel_stats(self):
         st = KernelStats()

@@ -30,6 +30,25 @@ def test_library_exports_every_header_symbol():
     assert f"#define DG_MAX_KERNEL_N {dg.MAX_KERNEL_N}" in hdr
 
 
+@pytest.mark.parametrize("prec", [4, 8])
+def test_kernel_config_matches_tune_table(prec):
+    """dg_get_kernel_config reports the knob set csrc/tune.json picked for each (N, precision)
+    (the library was built from that table), and shared memory fits one B200 SM."""
+    import json
+    tune = json.load(open(os.path.join(ROOT, "paper_1304_5546_b200", "csrc", "tune.json")))
+    VX, VY, E = dginputs.rect_mesh(1)
+    for N in range(1, dg.MAX_KERNEL_N + 1):
+        c = dg.dg_setup(N, VX, VY, E, device=-1, precision=prec)
+        k = c.kernel_config()
+        c.destroy()
+        t = tune[f"N{N}_{'f32' if prec == 4 else 'f64'}"]
+        want = ("3xtf32" if prec == 4 else "dmma_fp64") if t["M"] else "fma"
+        assert k["contraction"] == want, (N, k)
+        assert k["slots"] == t["S"] and k["teams_cap"] == t["C"]
+        assert k["residual_tma"] == bool(t["M"] and prec == 4 and t.get("Q", 1))
+        assert 0 < k["smem_bytes"] <= 227 * 1024 and k["threads"] % 32 == 0
+
+
 def _jittered(n, amp=0.25, seed=7, nx=None):
     VX, VY, E = dginputs.rect_mesh(n, nx)
     rng = np.random.default_rng(seed)

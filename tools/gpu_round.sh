@@ -1,6 +1,7 @@
 #!/bin/bash
-# One GPU pass for the round's evidence: bench lines (C4 fp32/fp64, C5), reference arm,
-# launch list of the default bench, full ncu of the fused kernel (5 stages = 1 LSERK4 step).
+# One GPU pass for the round's evidence: bench lines (C4 fp32/fp64, C5, C5w), reference arm,
+# launch list of the default bench, full ncu of the fused kernel (5 stages = 1 LSERK4 step)
+# for C4 fp32, C4 fp64 and C5 (N=8 fp64 two-layer material).
 mkdir -p gpurun_out
 python bench.py --steps 200 --warmup 10 > gpurun_out/bench.json 2> gpurun_out/bench.err
 python bench.py --steps 200 --warmup 10 --prec 8 --no-cpu-baseline > gpurun_out/bench_f64.json 2>> gpurun_out/bench.err
@@ -13,4 +14,6 @@ ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 
     python tools/prof_one.py 5 4 724 1 3 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 10 -c 5 -o gpurun_out/fused_n5_f64 \
     python tools/prof_one.py 5 8 724 1 3 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 10 -c 5 -o gpurun_out/fused_n8_f64_mat \
+    python tools/prof_mat.py 8 8 1448 3 > /dev/null 2>&1
 ls -la gpurun_out
