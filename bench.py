@@ -52,6 +52,28 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def compute_peak(prec, contraction):
+    """Measured arithmetic peak (TFLOP/s) of the pipe the contraction runs on, and its label:
+    FFMA / DFMA from profiles/r01_peaks_fma_hbm.json (tools/peaks.cu), mma.sync TF32 / DMMA
+    from profiles/r01_peaks_mma.json (tools/mma_peaks.cu).  3xTF32 issues 3 tensor products
+    per fp32 product, so its fp32-equivalent peak is the TF32 rate / 3."""
+    def load(name):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                return json.load(fh)
+        except Exception:
+            return {}
+    fma, mma = load("r01_peaks_fma_hbm.json"), load("r01_peaks_mma.json")
+    if contraction == "dmma_fp64":
+        return "tensor", float(mma.get("dmma_tflops", 36.0)), "measured DMMA m8n8k4 (tools/mma_peaks.cu)"
+    if contraction == "3xtf32":
+        return ("tensor", float(mma.get("tf32_tflops", 275.0)) / 3,
+                "measured TF32 mma.sync m16n8k8 / 3 (tools/mma_peaks.cu)")
+    if prec == 8:
+        return "alu", float(fma.get("dfma_reg_tflops", 35.45)), "measured DFMA (tools/peaks.cu)"
+    return "alu", float(fma.get("ffma_reg_tflops", 70.23)), "measured FFMA (tools/peaks.cu)"
+
+
 def algorithmic_bytes_per_element_stage(Np, s):
     """Bytes the method must move per element per LSERK4 stage, averaged over the 5 stages
     (DESIGN.md §Roofline): q_in read + q_out write (6 Np) + residual read on stages 1-4 and
@@ -274,11 +296,21 @@ def run_ours(args, rank, world, local_rank):
             traffic = tr
     except Exception:
         pass
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": traffic, "kernel": f"stage_kernel<{kind}>", "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": abytes, "avg_launch_ms": k_ms,
-            "flops_per_launch": flops_per_element_stage(args.order) * K_local,
-            "achieved_tflops": flops_per_element_stage(args.order) * K_local / (k_ms * 1e-3) / 1e12}
+    # the binding roof: HBM unless the arithmetic intensity exceeds the ridge of the pipe the
+    # contraction runs on (C5: N=8 fp64, 6.3 flop/B > 36 TF / 6.54 TB/s = 5.5)
+    flops = flops_per_element_stage(args.order) * K_local
+    tflops = flops / (k_ms * 1e-3) / 1e12
+    cbound, cpeak, csrc = compute_peak(s, kcfg["contraction"])
+    hbm_roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "peak_source": peak_src}
+    cmp_roof = {"bound": cbound, "achieved": tflops, "peak": cpeak, "unit": "TFLOP/s", "frac": tflops / cpeak,
+                "peak_source": csrc}
+    intensity = flops / abytes
+    main, alt = (cmp_roof, hbm_roof) if intensity > cpeak * 1e3 / hbm else (hbm_roof, cmp_roof)
+    roof = dict(main, traffic=traffic, kernel=f"stage_kernel<{kind}>", algorithmic_bytes_per_launch=abytes,
+                avg_launch_ms=k_ms, flops_per_launch=flops, achieved_tflops=tflops,
+                intensity_flop_per_byte=intensity, ridge_flop_per_byte=cpeak * 1e3 / hbm,
+                other_roof={k: alt[k] for k in ("bound", "achieved", "peak", "unit", "frac", "peak_source")})
     # e2e through the public API with host buffers (job level: set fields, K steps, get fields)
     barrier()
     outs = [torch.empty_like(a).pin_memory() for a in q0]
