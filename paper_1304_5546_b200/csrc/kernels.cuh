@@ -65,13 +65,15 @@ constexpr int TL = dg::TILE;
 constexpr bool USE_MMA = !F32 && DG_MMA;
 // fp32 only: the same contractions as 3xTF32 products on the tensor cores (mma.sync
 // m16n8k8: A = fields, elements x nodes; B = operator^T), split hi + lo so the result
-// keeps fp32 accuracy -- one 16-element m-tile per warp, two warps per tile
+// keeps fp32 accuracy -- DG_MMA=1: one 16-element m-tile per warp, two warps per tile;
+// DG_MMA=2: four warps, each an m-tile x one field set (Hx, Hy | Ez)
 constexpr bool USE_TF = F32 && DG_MMA;
+constexpr bool TF_SPLIT = USE_TF && DG_MMA == 2;  // 4 warps: m-tile x {Hx, Hy | Ez}
 #ifndef DG_R
 #define DG_R (sizeof(DG_T) == 4 ? 8 : 6)
 #endif
 constexpr int R_TARGET = USE_MMA ? 8 : DG_R;  // max rows per warp
-constexpr int P = USE_TF ? 2 : (NP + R_TARGET - 1) / R_TARGET;  // warps per tile
+constexpr int P = USE_TF ? (TF_SPLIT ? 4 : 2) : (NP + R_TARGET - 1) / R_TARGET;  // warps per tile
 constexpr int R = (NP + P - 1) / P;                // rows per warp
 constexpr int RP = P * R;                          // padded rows (extra rows are zero)
 constexpr int TEAM = P * 32;
@@ -391,19 +393,25 @@ __device__ __forceinline__ void tmma3(float (&c)[4], const uint32_t (&ah)[4], co
   tmma(c, ah, __float_as_uint(bh0), __float_as_uint(bh1));
 }
 
-// One tile on the 3xTF32 path (fp32): elements are the MMA rows -- warp g owns
-// elements e = 16g + lane/4 (+8) -- and each n-tile is 8 output rows, so the padding is
-// only Np -> 8 NT.  Volume (u = Dr Ez, v = Ds Ez, w = Dr W1 + Ds W2, as volume_rows)
-// -> flux (flux_points, one lane per element) -> LIFT -> material scaling -> LSERK4.
+// One tile on the 3xTF32 path (fp32): elements are the MMA rows -- the warp owns
+// elements e = 16 mt + lane/4 (+8) of m-tile mt -- and each n-tile is 8 output rows, so
+// the padding is only Np -> 8 NT.  Volume (u = Dr Ez, v = Ds Ez, w = Dr W1 + Ds W2, as
+// volume_rows) -> flux (flux_points, one lane per element, all P warps) -> LIFT ->
+// material scaling -> LSERK4.  FS selects the output fields the warp owns: 0 all three
+// (DG_MMA=1: P = 2 warps, one per m-tile), 1 = Hx, Hy (from u, v) and 2 = Ez (from w)
+// (DG_MMA=2: P = 4 warps, m-tile x field set: half the registers per warp, twice the warps).
 // C-fragment register r of n-tile nt is element ee[r >> 1], row 8nt + 2(lane%4) + (r & 1).
-template <int MODE, bool MAT, typename TT>
+template <int MODE, bool MAT, int FS, typename TT>
 __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
                                         TT* __restrict__ sp, const TT* __restrict__ sr,
                                         const unsigned char* __restrict__ ops, const int32_t (&vmc)[KPT],
-                                        int tile, int g, int lane, TT alpha, bool read_res) {
+                                        int tile, int g, int mt, int lane, TT alpha, bool read_res) {
   using MT = ModeTraits<MODE>;
+  constexpr int NFLD = FS == 0 ? 3 : (FS == 1 ? 2 : 1);  // output fields F0 .. F0 + NFLD - 1
+  constexpr int F0 = FS == 2 ? 2 : 0;
+  constexpr bool UV = FS != 2, WW = FS != 1;  // this warp forms u, v (Hx, Hy) / w (Ez)
   const int tig = lane & 3;
-  const int ee[2] = {16 * g + (lane >> 2), 16 * g + (lane >> 2) + 8};
+  const int ee[2] = {16 * mt + (lane >> 2), 16 * mt + (lane >> 2) + 8};
   // Lane-invariant shared-memory offsets.  A fragments read node rows 8ks + 4kh + tig, whose
   // swizzle (row & 3 = tig) does not depend on (ks, kh): row offsets are compile-time.  Rows
   // past Np / 3Nfp meet zero B rows; they read the next field, the geometry block (fields) or
@@ -417,7 +425,7 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
   }
   auto row_ok = [&](int nt, int r) { return NT * 8 == NP || nt < NT - 1 || 8 * nt + 2 * tig + (r & 1) < NP; };
   const int64_t tbase = (int64_t)tile * NP * TL;
-  TT acc[3][NT][4];
+  TT acc[NFLD][NT][4];  // acc[f]: field F0 + f
   if constexpr (MT::vol) {
     TT rxe[2], sxe[2], rye[2], sye[2];
 #pragma unroll
@@ -427,11 +435,13 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
       rye[i] = sg[2 * TL + ee[i]];
       sye[i] = sg[3 * TL + ee[i]];
     }
-    TT u[NT][4], v[NT][4];
+    // UV: u accumulates in acc[0], v in acc[1] (turned into rhsHx, rhsHy below); WW: w in acc[NFLD-1]
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int f = 0; f < NFLD; ++f)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) u[nt][r] = v[nt][r] = acc[2][nt][r] = TT(0);
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[f][nt][r] = TT(0);
     const float4* BV = reinterpret_cast<const float4*>(ops) + lane;
 #pragma unroll
     for (int ks = 0; ks < KVT; ++ks) {
@@ -440,29 +450,38 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
       for (int r = 0; r < 4; ++r) {  // A register r: element ee[r & 1], node 8ks + tig + 4(r >> 1)
         const int i = r & 1;
         const TT* a = sq + abase[i] + (8 * ks + 4 * (r >> 1)) * TL;
-        const TT hx = a[0], hy = a[NP * TL], ez = a[2 * NP * TL];
-        split_tf32(ez, ezh[r], ezl[r]);
-        split_tf32(rxe[i] * hy - rye[i] * hx, w1h[r], w1l[r]);
-        split_tf32(sxe[i] * hy - sye[i] * hx, w2h[r], w2l[r]);
+        if constexpr (UV) split_tf32(a[2 * NP * TL], ezh[r], ezl[r]);
+        if constexpr (WW) {
+          const TT hx = a[0], hy = a[NP * TL];
+          split_tf32(rxe[i] * hy - rye[i] * hx, w1h[r], w1l[r]);
+          split_tf32(sxe[i] * hy - sye[i] * hx, w2h[r], w2l[r]);
+        }
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const float4 bh = BV[(ks * NT + nt) * 64];  // hi and lo: 32 lanes x 16 B contiguous each
         const float4 bl = BV[(ks * NT + nt) * 64 + 32];
-        tmma3(u[nt], ezh, ezl, bh.x, bh.y, bl.x, bl.y);
-        tmma3(v[nt], ezh, ezl, bh.z, bh.w, bl.z, bl.w);
-        tmma3(acc[2][nt], w1h, w1l, bh.x, bh.y, bl.x, bl.y);
-        tmma3(acc[2][nt], w2h, w2l, bh.z, bh.w, bl.z, bl.w);
+        if constexpr (UV) {
+          tmma3(acc[0][nt], ezh, ezl, bh.x, bh.y, bl.x, bl.y);
+          tmma3(acc[1][nt], ezh, ezl, bh.z, bh.w, bl.z, bl.w);
+        }
+        if constexpr (WW) {
+          tmma3(acc[NFLD - 1][nt], w1h, w1l, bh.x, bh.y, bl.x, bl.y);
+          tmma3(acc[NFLD - 1][nt], w2h, w2l, bh.z, bh.w, bl.z, bl.w);
+        }
       }
     }
+    if constexpr (UV) {
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int i = r >> 1;
-        acc[0][nt][r] = -(rye[i] * u[nt][r] + sye[i] * v[nt][r]);
-        acc[1][nt][r] = rxe[i] * u[nt][r] + sxe[i] * v[nt][r];
-      }
+        for (int r = 0; r < 4; ++r) {
+          const int i = r >> 1;
+          const TT u = acc[0][nt][r], v = acc[1][nt][r];
+          acc[0][nt][r] = -(rye[i] * u + sye[i] * v);
+          acc[1][nt][r] = rxe[i] * u + sxe[i] * v;
+        }
+    }
   } else if constexpr (MODE == dg::MODE_SURFACE_RK) {
     const TT* __restrict__ rv = static_cast<const TT*>(p.rhsv) + tbase;
 #pragma unroll
@@ -470,18 +489,18 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          acc[c][nt][r] = row_ok(nt, r) ? rv[c * p.vstride + 8 * nt * TL + cbase[r]] : TT(0);
+        for (int f = 0; f < NFLD; ++f)
+          acc[f][nt][r] = row_ok(nt, r) ? rv[(F0 + f) * p.vstride + 8 * nt * TL + cbase[r]] : TT(0);
   } else {
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
+    for (int f = 0; f < NFLD; ++f)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) acc[c][nt][r] = TT(0);
+        for (int r = 0; r < 4; ++r) acc[f][nt][r] = TT(0);
   }
   // LSERK4 residual -> registers (DG_RT=0; in flight during the surface phase)
-  TT rr[3][NT][4];
+  TT rr[NFLD][NT][4];
   if constexpr (MT::rk && !RES_TMA) {
     if (read_res) {
       const TT* __restrict__ res = static_cast<const TT*>(p.res) + tbase;
@@ -490,8 +509,8 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 3; ++c)
-            rr[c][nt][r] = row_ok(nt, r) ? __ldcs(res + c * p.vstride + 8 * nt * TL + cbase[r]) : TT(0);
+          for (int f = 0; f < NFLD; ++f)
+            rr[f][nt][r] = row_ok(nt, r) ? __ldcs(res + (F0 + f) * p.vstride + 8 * nt * TL + cbase[r]) : TT(0);
     }
   }
   if constexpr (MT::surf) {
@@ -500,18 +519,18 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
     const float4* BL = reinterpret_cast<const float4*>(ops + DVB) + lane;
 #pragma unroll
     for (int ks = 0; ks < KLT; ++ks) {
-      uint32_t fh[3][4], fl[3][4];
+      uint32_t fh[NFLD][4], fl[NFLD][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const TT* a = sp + abase[r & 1] + (8 * ks + 4 * (r >> 1)) * TL;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) split_tf32(a[c * NFE * TL], fh[c][r], fl[c][r]);
+        for (int f = 0; f < NFLD; ++f) split_tf32(a[(F0 + f) * NFE * TL], fh[f][r], fl[f][r]);
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const float4 b = BL[(ks * NT + nt) * 32];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) tmma3(acc[c][nt], fh[c], fl[c], b.x, b.y, b.z, b.w);
+        for (int f = 0; f < NFLD; ++f) tmma3(acc[f][nt], fh[f], fl[f], b.x, b.y, b.z, b.w);
       }
     }
   }
@@ -521,13 +540,11 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
       for (int i = 0; i < 2; ++i) {
         const TT imu = sg[16 * TL + ee[i]], ieps = sg[17 * TL + ee[i]];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int f = 0; f < NFLD; ++f)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            acc[0][nt][2 * i + h] *= imu;
-            acc[1][nt][2 * i + h] *= imu;
-            acc[2][nt][2 * i + h] *= ieps;
-          }
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) acc[f][nt][2 * i + h] *= (F0 + f == 2 ? ieps : imu);
       }
     }
   }
@@ -542,16 +559,17 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
         TT* __restrict__ res = static_cast<TT*>(p.res) + tbase;
         TT* __restrict__ qo = static_cast<TT*>(p.q_out) + tbase;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          TT rs = dt * acc[c][nt][r];
-          if (read_res) rs = fma(a, RES_TMA ? sr[c * NP * TL + o] : rr[c][nt][r], rs);
+        for (int f = 0; f < NFLD; ++f) {
+          const int c = F0 + f;
+          TT rs = dt * acc[f][nt][r];
+          if (read_res) rs = fma(a, RES_TMA ? sr[c * NP * TL + o] : rr[f][nt][r], rs);
           if (p.write_res) __stcs(res + c * p.vstride + o, rs);
           __stcs(qo + c * p.fstride + o, fma(b, rs, sq[c * NP * TL + o]));
         }
       } else {
         TT* __restrict__ out = static_cast<TT*>(p.out) + tbase;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) out[c * p.vstride + o] = acc[c][nt][r];
+        for (int f = 0; f < NFLD; ++f) out[(F0 + f) * p.vstride + o] = acc[f][nt][r];
       }
     }
 }
@@ -840,7 +858,14 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     if constexpr (USE_MMA) {
       mma_tile<MODE, MAT>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, lane, alpha, read_res);
     } else if constexpr (USE_TF) {
-      tf_tile<MODE, MAT>(p, sq, sg_of(s), sp, sr_of(s), smem_raw + BARB, vc0, tile, g, lane, alpha, read_res);
+      if constexpr (TF_SPLIT) {
+        if (g < 2)
+          tf_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, sr_of(s), smem_raw + BARB, vc0, tile, g, g & 1, lane, alpha, read_res);
+        else
+          tf_tile<MODE, MAT, 2>(p, sq, sg_of(s), sp, sr_of(s), smem_raw + BARB, vc0, tile, g, g & 1, lane, alpha, read_res);
+      } else {
+        tf_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, sr_of(s), smem_raw + BARB, vc0, tile, g, g, lane, alpha, read_res);
+      }
     } else {
     T rhx[R], rhy[R], rez[R];
     if constexpr (MT::vol) {
