@@ -69,11 +69,14 @@ constexpr bool USE_MMA = !F32 && DG_MMA;
 // DG_MMA=2: four warps, each an m-tile x one field set (Hx, Hy | Ez)
 constexpr bool USE_TF = F32 && DG_MMA;
 constexpr bool TF_SPLIT = USE_TF && DG_MMA == 2;  // 4 warps: m-tile x {Hx, Hy | Ez}
+constexpr bool DMMA_SPLIT = USE_MMA && DG_MMA == 2;  // 2 PR warps: row group x {Hx, Hy | Ez}
+constexpr int PR = (NP + 7) / 8;                     // DMMA row groups (8 output rows each)
 #ifndef DG_R
 #define DG_R (sizeof(DG_T) == 4 ? 8 : 6)
 #endif
 constexpr int R_TARGET = USE_MMA ? 8 : DG_R;  // max rows per warp
-constexpr int P = USE_TF ? (TF_SPLIT ? 4 : 2) : (NP + R_TARGET - 1) / R_TARGET;  // warps per tile
+constexpr int P = USE_TF ? (TF_SPLIT ? 4 : 2)
+                          : USE_MMA ? (DMMA_SPLIT ? 2 * PR : PR) : (NP + R_TARGET - 1) / R_TARGET;  // warps per tile
 constexpr int R = (NP + P - 1) / P;                // rows per warp
 constexpr int RP = P * R;                          // padded rows (extra rows are zero)
 constexpr int TEAM = P * 32;
@@ -102,9 +105,9 @@ constexpr int KVT = (NP + 7) / 8;  // TF32 k-steps of the volume contraction
 constexpr int KLT = (NF + 7) / 8;  // TF32 k-steps of the LIFT contraction
 constexpr int RPL = (RP + 1) & ~1;  // LIFT rows padded to even
 constexpr size_t DVB = USE_TF ? (size_t)KVT * NT * 32 * 32
-                              : USE_MMA ? (size_t)KV * P * 32 * 16 : (size_t)NPC * RP * 2 * VC * sizeof(T);
+                              : USE_MMA ? (size_t)KV * PR * 32 * 16 : (size_t)NPC * RP * 2 * VC * sizeof(T);
 constexpr size_t LVB = USE_TF ? (size_t)KLT * NT * 32 * 16
-                              : USE_MMA ? (size_t)KL * P * 32 * 8 : (size_t)NFC * RPL * VC * sizeof(T);
+                              : USE_MMA ? (size_t)KL * PR * 32 * 8 : (size_t)NFC * RPL * VC * sizeof(T);
 constexpr size_t OPB = ((DVB + LVB + 15) / 16) * 16;
 // Column swizzle of the tile-blocked layout: element e of node row n is stored at
 // column e ^ (SWM * (n & 3)).  Identity for the FMA kernels; for the DMMA kernels
@@ -308,11 +311,12 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "d"(a), "d"(b));
 }
 
-// Volume term of one tile on the tensor cores: warp g owns rows [8g, 8g+8), the
+// Volume term of one tile on the tensor cores: warp row group g owns rows [8g, 8g+8), the
 // four 8-element n-tiles of the tile are the columns.  u = Dr Ez, v = Ds Ez,
 // w = Dr W1 + Ds W2 with W1 = rx Hy - ry Hx, W2 = sx Hy - sy Hx per element
-// (same algebra as volume_rows), accumulated over KV k-steps of 4 nodes.
-template <typename AVT>
+// (same algebra as volume_rows), accumulated over KV k-steps of 4 nodes.  Field set FS
+// (as tf_tile): 0 all, 1 only u, v (-> Hx, Hy), 2 only w (-> Ez).
+template <int FS, typename AVT>
 __device__ __forceinline__ void volume_mma(const double* __restrict__ sq, const double* __restrict__ sg,
                                            const AVT* __restrict__ AV, int g, int lane, double (&u)[4][2],
                                            double (&v)[4][2], double (&w)[4][2]) {
@@ -326,22 +330,26 @@ __device__ __forceinline__ void volume_mma(const double* __restrict__ sq, const 
     syb[nt] = sg[3 * TL + eb];
     u[nt][0] = u[nt][1] = v[nt][0] = v[nt][1] = w[nt][0] = w[nt][1] = 0.0;
   }
+  constexpr bool UV = FS != 2, WW = FS != 1;
   double w2acc[4][2] = {};  // Ds W2 in its own accumulator: 4 independent DMMA chains per n-tile
 #pragma unroll
   for (int ks = 0; ks < KV; ++ks) {
     const int j = 4 * ks + (lane & 3);
     const int jc = j < NP ? j : NP - 1;  // padded k rows: A is zero there
-    const AVT a = AV[(ks * P + g) * 32 + lane];
+    const AVT a = AV[(ks * PR + g) * 32 + lane];
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int addr = jc * TL + colx(jc, 8 * nt + (lane >> 2));
-      const double hx = sq[0 * NP * TL + addr], hy = sq[1 * NP * TL + addr], ez = sq[2 * NP * TL + addr];
-      const double w1 = rxb[nt] * hy - ryb[nt] * hx;
-      const double w2 = sxb[nt] * hy - syb[nt] * hx;
-      dmma(u[nt][0], u[nt][1], a.x, ez);
-      dmma(v[nt][0], v[nt][1], a.y, ez);
-      dmma(w[nt][0], w[nt][1], a.x, w1);
-      dmma(w2acc[nt][0], w2acc[nt][1], a.y, w2);
+      if constexpr (UV) {
+        const double ez = sq[2 * NP * TL + addr];
+        dmma(u[nt][0], u[nt][1], a.x, ez);
+        dmma(v[nt][0], v[nt][1], a.y, ez);
+      }
+      if constexpr (WW) {
+        const double hx = sq[0 * NP * TL + addr], hy = sq[1 * NP * TL + addr];
+        dmma(w[nt][0], w[nt][1], a.x, rxb[nt] * hy - ryb[nt] * hx);
+        dmma(w2acc[nt][0], w2acc[nt][1], a.y, sxb[nt] * hy - syb[nt] * hx);
+      }
     }
   }
 #pragma unroll
@@ -351,20 +359,23 @@ __device__ __forceinline__ void volume_mma(const double* __restrict__ sq, const 
   }
 }
 
-// rhs += LIFT f on the tensor cores (f in sp, swizzled [c][NF][32]).
+// rhs += LIFT f on the tensor cores (f in sp, swizzled [c][NF][32]); fields of set FS.
+template <int FS>
 __device__ __forceinline__ void lift_mma(const double* __restrict__ sp, const double* __restrict__ AL, int g,
                                          int lane, double (&rhx)[4][2], double (&rhy)[4][2], double (&rez)[4][2]) {
 #pragma unroll
   for (int ks = 0; ks < KL; ++ks) {
     const int m = 4 * ks + (lane & 3);
     const int mc = m < NF ? m : NF - 1;
-    const double a = AL[(ks * P + g) * 32 + lane];
+    const double a = AL[(ks * PR + g) * 32 + lane];
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int addr = mc * TL + colx(mc, 8 * nt + (lane >> 2));
-      dmma(rhx[nt][0], rhx[nt][1], a, sp[0 * NFE * TL + addr]);
-      dmma(rhy[nt][0], rhy[nt][1], a, sp[1 * NFE * TL + addr]);
-      dmma(rez[nt][0], rez[nt][1], a, sp[2 * NFE * TL + addr]);
+      if constexpr (FS != 2) {
+        dmma(rhx[nt][0], rhx[nt][1], a, sp[0 * NFE * TL + addr]);
+        dmma(rhy[nt][0], rhy[nt][1], a, sp[1 * NFE * TL + addr]);
+      }
+      if constexpr (FS != 1) dmma(rez[nt][0], rez[nt][1], a, sp[2 * NFE * TL + addr]);
     }
   }
 }
@@ -613,22 +624,24 @@ __device__ __forceinline__ void lift_rows(const T* __restrict__ sp, const LVT* _
 
 // One tile on the DMMA path (fp64): volume (tensor cores) -> flux (one lane per
 // element, as the FMA path) -> LIFT (tensor cores) -> material scaling -> LSERK4
-// update.  Each lane owns C-fragment rows n = 8g + lane/4 and the element pairs
-// e = 8nt + 2(lane%4) + {0,1}; stores are 16 B pairs (e, e+1 stay adjacent under
-// the column swizzle).
-template <int MODE, bool MAT, typename TT>
+// update.  Each lane owns C-fragment rows n = 8 rg + lane/4 (rg = the warp's row group)
+// and the element pairs e = 8nt + 2(lane%4) + {0,1}; stores are 16 B pairs (e, e+1 stay
+// adjacent under the column swizzle).  FS = field set (volume_mma): DG_MMA=2 gives each
+// row group two warps, one for Hx, Hy and one for Ez.
+template <int MODE, bool MAT, int FS, typename TT>
 __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
                                          TT* __restrict__ sp, const unsigned char* __restrict__ ops,
-                                         const int32_t (&vmc)[KPT], int tile, int g, int lane, TT alpha,
+                                         const int32_t (&vmc)[KPT], int tile, int g, int rg, int lane, TT alpha,
                                          bool read_res) {
   using MT = ModeTraits<MODE>;
   using V2 = typename std::conditional<sizeof(TT) == 8, double2, float2>::type;
-  const int n = 8 * g + (lane >> 2);  // this lane's output row
+  constexpr bool ACT[3] = {FS != 2, FS != 2, FS != 1};  // output fields of this warp
+  const int n = 8 * rg + (lane >> 2);  // this lane's output row
   const int nc = n < NP ? n : NP - 1;
   TT rhx[4][2], rhy[4][2], rez[4][2];
   if constexpr (MT::vol) {
     TT u[4][2], v[4][2];
-    volume_mma(sq, sg, reinterpret_cast<const V2*>(ops), g, lane, u, v, rez);
+    volume_mma<FS>(sq, sg, reinterpret_cast<const V2*>(ops), rg, lane, u, v, rez);
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -665,14 +678,15 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
       for (int nt = 0; nt < 4; ++nt) {
         const int64_t off = ((int64_t)tile * NP + nc) * TL + colx(nc, 8 * nt + 2 * (lane & 3));
 #pragma unroll
-        for (int c = 0; c < 3; ++c) rr[c][nt] = __ldcs(reinterpret_cast<const V2*>(res + c * p.vstride + off));
+        for (int c = 0; c < 3; ++c)
+          if (ACT[c]) rr[c][nt] = __ldcs(reinterpret_cast<const V2*>(res + c * p.vstride + off));
       }
     }
   }
   if constexpr (MT::surf) {
     flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
     __syncthreads();
-    lift_mma(sp, reinterpret_cast<const TT*>(ops + DVB), g, lane, rhx, rhy, rez);
+    lift_mma<FS>(sp, reinterpret_cast<const TT*>(ops + DVB), rg, lane, rhx, rhy, rez);
   }
   if constexpr (MAT) {
     if (MODE != dg::MODE_VOLUME || p.scale_volume) {
@@ -700,6 +714,7 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
       const TT a = static_cast<TT>(p.a), b = static_cast<TT>(p.b), dt = static_cast<TT>(p.dt);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
+        if (!ACT[c]) continue;
         V2 rs;
         rs.x = dt * r3[c][0];
         rs.y = dt * r3[c][1];
@@ -718,6 +733,7 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
       TT* __restrict__ out = static_cast<TT*>(p.out);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
+        if (!ACT[c]) continue;
         V2 o;
         o.x = r3[c][0];
         o.y = r3[c][1];
@@ -856,7 +872,14 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     const T* gg = sg_of(s) + lane;
     T* sp = sp_of(s);
     if constexpr (USE_MMA) {
-      mma_tile<MODE, MAT>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, lane, alpha, read_res);
+      if constexpr (DMMA_SPLIT) {
+        if (g < PR)
+          mma_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, g, lane, alpha, read_res);
+        else
+          mma_tile<MODE, MAT, 2>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, g - PR, lane, alpha, read_res);
+      } else {
+        mma_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, g, lane, alpha, read_res);
+      }
     } else if constexpr (USE_TF) {
       if constexpr (TF_SPLIT) {
         if (g < 2)
@@ -1009,12 +1032,12 @@ void pack_ops(const double* Dr, const double* Ds, const double* LIFT, void* out)
   if constexpr (USE_MMA) {  // A fragments: lane -> (row 8g + lane/4, column 4k + lane%4)
     T* av = reinterpret_cast<T*>(o);
     T* al = reinterpret_cast<T*>(o + DVB);
-    for (int g = 0; g < P; ++g)
+    for (int g = 0; g < PR; ++g)
       for (int ln = 0; ln < 32; ++ln) {
         const int n = 8 * g + ln / 4;
         for (int ks = 0; ks < KV; ++ks) {
           const int j = 4 * ks + ln % 4;
-          T* e = av + ((size_t)(ks * P + g) * 32 + ln) * 2;
+          T* e = av + ((size_t)(ks * PR + g) * 32 + ln) * 2;
           if (n < NP && j < NP) {
             e[0] = static_cast<T>(Dr[n * NP + j]);
             e[1] = static_cast<T>(Ds[n * NP + j]);
@@ -1022,7 +1045,7 @@ void pack_ops(const double* Dr, const double* Ds, const double* LIFT, void* out)
         }
         for (int ks = 0; ks < KL; ++ks) {
           const int m = 4 * ks + ln % 4;
-          if (n < NP && m < NF) al[(size_t)(ks * P + g) * 32 + ln] = static_cast<T>(LIFT[n * NF + m]);
+          if (n < NP && m < NF) al[(size_t)(ks * PR + g) * 32 + ln] = static_cast<T>(LIFT[n * NF + m]);
         }
       }
     return;
