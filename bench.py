@@ -252,8 +252,10 @@ def run_ours(args, rank, world, local_rank):
     # warm-up
     ctx.run(dt, args.warmup)
     ctx.sync()
-    # timed region: exactly K steps, kernel events on the library's stream
+    # timed region: exactly K steps as dg_run runs them (CUDA-graph replay), events on the
+    # library's stream; the statistics reset first so gpu_launches counts this region only
     ctx.profile(True)
+    ctx.profile(False)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
@@ -268,8 +270,13 @@ def run_ours(args, rank, world, local_rank):
         t_wall = time.perf_counter() - t_wall
         barrier()
     ms = e0.elapsed_time(e1)
-    stats = ctx.kernel_stats()
+    launches = sum(v["launches"] for v in ctx.kernel_stats().values())
     kcfg = ctx.kernel_config()
+    ctx.sync()
+    # per-launch kernel durations (roofline): a separate eagerly launched, event-bracketed pass
+    ctx.profile(True)
+    ctx.run(dt, min(args.steps, 20))
+    stats = ctx.kernel_stats()
     ctx.profile(False)
     ctx.sync()
     if dist is not None:
@@ -279,7 +286,6 @@ def run_ours(args, rank, world, local_rank):
     value = Np * K * 3 * 5 * args.steps / (ms * 1e-3)
     # dominant kernel roofline
     kind = "volume" if args.split else "fused"
-    launches = sum(v["launches"] for v in stats.values())
     s = args.prec
     hbm, peak_src = peaks()
     if args.split:

@@ -178,6 +178,13 @@ typedef struct {
   int64_t timed[4];      /* launches that were event-timed */
 } dg_kernel_stats;
 
+/* CUDA graphs for dg_run (single-rank contexts; default on): after one eager step, each
+ * LSERK4 step (its 5 stage launches) is captured once per ping-pong parity for the current
+ * dt and replayed with cudaGraphLaunch -- the same kernels and arguments, bitwise the same
+ * result.  A new dt recaptures.  Profiling (dg_profile) runs eagerly.  0 disables (and
+ * frees the graphs after synchronising the stream). */
+dg_status dg_set_graphs(dg_ctx* c, int32_t enable);
+
 /* Turn per-launch CUDA-event timing on (1) or off (0); resets the statistics. */
 dg_status dg_profile(dg_ctx* c, int32_t enable);
 

@@ -200,6 +200,11 @@ struct dg_ctx {
   bool own_stream = false;
   cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
   ncclComm_t nccl_comm = nullptr;
+  // CUDA graphs: one LSERK4 step (5 stages) per graph, one per starting ping-pong parity,
+  // captured for the current dt (single-rank contexts; eager while profiling)
+  bool graphs = true;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  double gdt = 0.0;
   // profiling
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -695,6 +700,37 @@ dg_status dg_get_fields(dg_ctx* c, double* Hx, double* Hy, double* Ez) {
   return DG_OK;
 }
 
+static void drop_graphs(dg_ctx* c) {
+  for (auto& g : c->gexec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+}
+
+// Capture one LSERK4 step starting from q[parity] (the same launches run_stage enqueues)
+static dg_status capture_step(dg_ctx* c, double dt, int parity) {
+  const int cur0 = c->cur;
+  const dg_kernel_stats st0 = c->stats;
+  c->cur = parity;
+  CU(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  dg_status st = DG_OK;
+  for (int i = 0; i < 5 && st == DG_OK; ++i) st = run_stage(c, i, dt);
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+  c->cur = cur0;
+  c->stats = st0;
+  if (st != DG_OK) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamEndCapture");
+  const cudaError_t e2 = cudaGraphInstantiate(&c->gexec[parity], g, 0);
+  cudaGraphDestroy(g);
+  if (e2 != cudaSuccess) return cuda_fail(c, e2, "cudaGraphInstantiate");
+  return DG_OK;
+}
+
 dg_status dg_run(dg_ctx* c, double dt, int64_t nsteps) {
   dg_status st = check_usable(c, true);
   if (st != DG_OK) return st;
@@ -702,9 +738,34 @@ dg_status dg_run(dg_ctx* c, double dt, int64_t nsteps) {
   if (c->transport == 1 && c->nranks > 1) return set_err(DG_E_STATE, "in-process group contexts run via dg_run_group");
   CU(c, cudaSetDevice(c->device));
   for (int64_t s = 0; s < nsteps; ++s) {
-    for (int i = 0; i < 5; ++i)
-      if ((st = run_stage(c, i, dt)) != DG_OK) return st;
+    // graph replay once a step has run eagerly (kernel attributes set up outside any capture)
+    if (c->graphs && c->nranks == 1 && !c->profiling && c->steps_done > 0) {
+      if (c->gdt != dt) {
+        drop_graphs(c);
+        c->gdt = dt;
+      }
+      if (!c->gexec[c->cur] && (st = capture_step(c, dt, c->cur)) != DG_OK) return st;
+      CU(c, cudaGraphLaunch(c->gexec[c->cur], c->stream));
+      c->stats.launches[c->fused ? 0 : 1] += 5;
+      if (!c->fused) c->stats.launches[2] += 5;
+      c->cur = 1 - c->cur;  // five stages: five ping-pong flips
+    } else {
+      for (int i = 0; i < 5; ++i)
+        if ((st = run_stage(c, i, dt)) != DG_OK) return st;
+    }
     ++c->steps_done;
+  }
+  return DG_OK;
+}
+
+dg_status dg_set_graphs(dg_ctx* c, int32_t enable) {
+  dg_status st = check_usable(c, true);
+  if (st != DG_OK) return st;
+  c->graphs = enable != 0;
+  if (!c->graphs) {
+    CU(c, cudaSetDevice(c->device));
+    CU(c, cudaStreamSynchronize(c->stream));
+    drop_graphs(c);
   }
   return DG_OK;
 }
@@ -979,6 +1040,7 @@ void dg_destroy(dg_ctx* c) {
   if (!c->host_only) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    drop_graphs(c);
     if (c->nccl_comm) {
       Nccl* n = nccl();
       if (n) (c->poisoned ? n->CommAbort : n->CommDestroy)(c->nccl_comm);

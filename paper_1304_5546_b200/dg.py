@@ -32,7 +32,7 @@ STATUS = {0: "DG_OK", 1: "DG_E_ARG", 2: "DG_E_DEGREE", 3: "DG_E_MESH_DEGENERATE"
 EXPORTS = ["dg_options_default", "dg_setup", "dg_sizes", "dg_local_elements", "dg_set_fields",
            "dg_get_fields", "dg_run", "dg_run_group", "dg_sync", "dg_eval_rhs", "dg_energy",
            "dg_get_operators", "dg_get_geometry", "dg_get_maps", "dg_get_nodes", "dg_halo_sizes",
-           "dg_get_halo", "dg_stream", "dg_profile", "dg_get_kernel_stats", "dg_get_kernel_config",
+           "dg_get_halo", "dg_stream", "dg_profile", "dg_get_kernel_stats", "dg_get_kernel_config", "dg_set_graphs",
            "dg_destroy", "dg_last_error"]
 
 
@@ -90,6 +90,7 @@ _sig = {
     "dg_profile": [_vp, C.c_int32],
     "dg_get_kernel_stats": [_vp, _vp],
     "dg_get_kernel_config": [_vp, _vp],
+    "dg_set_graphs": [_vp, C.c_int32],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -265,6 +266,10 @@ class Context:
         s = C.c_void_p()
         _check(_lib.dg_stream(self._h, C.byref(s)))
         return s.value
+
+    def set_graphs(self, enable=True):
+        """dg_set_graphs: replay dg_run's steps as CUDA graphs (default on)."""
+        _check(_lib.dg_set_graphs(self._h, 1 if enable else 0))
 
     def profile(self, enable=True):
         _check(_lib.dg_profile(self._h, 1 if enable else 0))
