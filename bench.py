@@ -74,21 +74,31 @@ def compute_peak(prec, contraction):
     return "alu", float(fma.get("ffma_reg_tflops", 70.23)), "measured FFMA (tools/peaks.cu)"
 
 
-def algorithmic_bytes_per_element_stage(Np, s):
+def algorithmic_bytes_per_element_stage(Np, s, kind="fused"):
     """Bytes the method must move per element per LSERK4 stage, averaged over the 5 stages
-    (DESIGN.md §Roofline): q_in read + q_out write (6 Np) + residual read on stages 1-4 and
-    write on stages 0-3 (2 * 0.8 * 3 Np) in the arithmetic type (s bytes), + 13 geometry words
+    (DESIGN.md §Roofline).  fused: q_in read + q_out write (6 Np) + residual read on stages 1-4
+    and write on stages 0-3 (2 * 0.8 * 3 Np) in the arithmetic type (s bytes), + 13 geometry words
     (rx, sx, ry, sy; nx, ny, Fsc per face) in the arithmetic type + 4 words of connectivity
-    (3 neighbour ids + packed face ids).  Neighbour traces are L2 hits (not DRAM)."""
+    (3 neighbour ids + packed face ids).  Neighbour traces are L2 hits (not DRAM).
+    Split variant: volume = q read + rhsV write (6 Np) + rx, sx, ry, sy; surface = q read,
+    rhsV read, q_out write (9 Np) + the residual (4.8 Np) + 9 face words + connectivity."""
+    if kind == "volume":
+        return 6.0 * Np * s + 4 * s
+    if kind == "surface":
+        return (9.0 + 4.8) * Np * s + 9 * s + 16
     return (6.0 + 4.8) * Np * s + 13 * s + 16
 
 
-def flops_per_element_stage(N):
+def flops_per_element_stage(N, kind="fused"):
     Np, Nfp = (N + 1) * (N + 2) // 2, N + 1
     vol = 8 * Np * Np + 8 * Np            # 4 mat-vecs (FMA = 2) + chain rule / curl
     lift = 2 * 3 * Np * 3 * Nfp           # LIFT on 3 fields
     flux = 3 * Nfp * 3 * 12               # jumps + upwind flux per face point
     rk = 3 * Np * 4                       # res = a res + dt rhs; q += b res
+    if kind == "volume":
+        return vol
+    if kind == "surface":
+        return lift + flux + rk + 3 * Np  # + rhsV added
     return vol + lift + flux + rk
 
 
@@ -284,39 +294,43 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = Np * K * 3 * 5 * args.steps / (ms * 1e-3)
-    # dominant kernel roofline
-    kind = "volume" if args.split else "fused"
     s = args.prec
     hbm, peak_src = peaks()
-    if args.split:
-        # split mode: report the surface+RK kernel (the larger share) separately in config
-        kind = max(("volume", "surface"), key=lambda k: stats[k]["ms"])
-    k_ms = stats[kind]["ms"] / max(stats[kind]["timed"], 1)
     K_local = ctx.K_local
-    abytes = algorithmic_bytes_per_element_stage(Np, s) * K_local
-    achieved = abytes / (k_ms * 1e-3) / 1e9
-    traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            tr = json.load(fh).get(f"N{args.order}_p{s}_n{args.n}_P{world}_{kind}")
-            traffic = tr
+            traffic_tab = json.load(fh)
     except Exception:
-        pass
-    # the binding roof: HBM unless the arithmetic intensity exceeds the ridge of the pipe the
-    # contraction runs on (C5: N=8 fp64, 6.3 flop/B > 36 TF / 6.54 TB/s = 5.5)
-    flops = flops_per_element_stage(args.order) * K_local
-    tflops = flops / (k_ms * 1e-3) / 1e12
-    cbound, cpeak, csrc = compute_peak(s, kcfg["contraction"])
-    hbm_roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "peak_source": peak_src}
-    cmp_roof = {"bound": cbound, "achieved": tflops, "peak": cpeak, "unit": "TFLOP/s", "frac": tflops / cpeak,
-                "peak_source": csrc}
-    intensity = flops / abytes
-    main, alt = (cmp_roof, hbm_roof) if intensity > cpeak * 1e3 / hbm else (hbm_roof, cmp_roof)
-    roof = dict(main, traffic=traffic, kernel=f"stage_kernel<{kind}>", algorithmic_bytes_per_launch=abytes,
-                avg_launch_ms=k_ms, flops_per_launch=flops, achieved_tflops=tflops,
-                intensity_flop_per_byte=intensity, ridge_flop_per_byte=cpeak * 1e3 / hbm,
-                other_roof={k: alt[k] for k in ("bound", "achieved", "peak", "unit", "frac", "peak_source")})
+        traffic_tab = {}
+
+    def roofline(kind):
+        """Roofline of one stage kernel: algorithmic bytes and flops per launch over its average
+        event-timed launch.  The binding roof is HBM unless the arithmetic intensity exceeds the
+        ridge of the pipe the contraction runs on (C5: N=8 fp64, 6.3 flop/B > 36 TF / 6.54 TB/s)."""
+        k_ms = stats[kind]["ms"] / max(stats[kind]["timed"], 1)
+        abytes = algorithmic_bytes_per_element_stage(Np, s, kind) * K_local
+        flops = flops_per_element_stage(args.order, kind) * K_local
+        achieved = abytes / (k_ms * 1e-3) / 1e9
+        tflops = flops / (k_ms * 1e-3) / 1e12
+        cbound, cpeak, csrc = compute_peak(s, kcfg["contraction"])
+        hbm_roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "peak_source": peak_src}
+        cmp_roof = {"bound": cbound, "achieved": tflops, "peak": cpeak, "unit": "TFLOP/s",
+                    "frac": tflops / cpeak, "peak_source": csrc}
+        intensity = flops / abytes
+        main, alt = (cmp_roof, hbm_roof) if intensity > cpeak * 1e3 / hbm else (hbm_roof, cmp_roof)
+        return dict(main, traffic=traffic_tab.get(f"N{args.order}_p{s}_n{args.n}_P{world}_{kind}"),
+                    kernel=f"stage_kernel<{kind}>", algorithmic_bytes_per_launch=abytes, avg_launch_ms=k_ms,
+                    flops_per_launch=flops, achieved_tflops=tflops, intensity_flop_per_byte=intensity,
+                    ridge_flop_per_byte=cpeak * 1e3 / hbm,
+                    other_roof={k: alt[k] for k in ("bound", "achieved", "peak", "unit", "frac", "peak_source")})
+
+    if args.split:  # the dominant (longer) kernel; the other one alongside
+        kinds = sorted(("volume", "surface"), key=lambda k: -stats[k]["ms"])
+        roof = roofline(kinds[0])
+        roof["second_kernel"] = roofline(kinds[1])
+    else:
+        roof = roofline("fused")
     # e2e through the public API with host buffers (job level: set fields, K steps, get fields)
     barrier()
     outs = [torch.empty_like(a).pin_memory() for a in q0]
