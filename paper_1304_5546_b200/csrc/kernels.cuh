@@ -5,20 +5,23 @@
 // so every (N, T) gets kernels with compile-time sizes (the paper's run-time
 // code generation, done as C++ templates).
 //
-// Work decomposition (DESIGN.md §Kernels):
-//   * one warp lane per element; a 32-element tile is owned by a "team" of
-//     P warps (one team per CTA), warp g computing output rows [gR, gR+R);
+// Work decomposition (DESIGN.md §6):
+//   * a 32-element tile is owned by a "team" of P warps (one team per CTA);
+//     the volume and LIFT contractions run on one of three paths (DG_MMA):
+//     FMA (one lane per element, warp g computing output rows [gR, gR+R)),
+//     fp64 DMMA (mma.sync m8n8k4, 8 rows per warp) or fp32 3xTF32 (mma.sync
+//     m16n8k8 with elements as M, hi/lo operand split);
 //   * tile-blocked field layout (kernel_api.h): every warp access to node n of
-//     a tile is one contiguous 128 B / 256 B line, and a thread reading its
-//     element's column out of shared memory is bank-conflict free;
-//   * operators in shared memory ("matrix-in-local"), laid
-//     out so that one broadcast LDS.128 feeds 8 FFMA (fp32: Dr,Ds of two
-//     columns) or 4 DFMA (fp64); LIFT as (column pairs | columns) per row;
-//   * persistent CTAs walk their tiles with a cp.async software pipeline:
-//     while tile t is computed out of one shared-memory slot, tile t+1's
-//     Hx, Hy, Ez (16 B copies), geometry block and neighbour traces q[vmapP]
-//     (4/8 B gathers, mostly L2 hits; vmapP fetched one tile earlier) land in
-//     the other slot, and tile t's LSERK4 residual lands in its own buffer.
+//     a tile is one contiguous 128 B / 256 B line; a per-path column swizzle
+//     keeps the shared-memory fragment loads bank-conflict free;
+//   * operators in shared memory ("matrix-in-local"), packed
+//     per path: broadcast LDS.128 rows (FMA) or per-lane MMA fragments;
+//   * persistent CTAs walk their tiles through S shared-memory slots: TMA bulk
+//     copies (cp.async.bulk + mbarrier) bring a tile's Hx, Hy, Ez, geometry
+//     (and, DG_RT, residual); cp.async gathers bring cross-tile neighbour
+//     traces q[vmapP] (same-tile ones are read from shared memory; vmapP is
+//     fetched two tiles ahead); with one slot the next tile's TMA sources are
+//     prefetched into L2 (cp.async.bulk.prefetch.L2) while the tile computes.
 //
 // Per tile, per stage (eq. 9 with readings A1/A2; eq. 6 chain
 // rule; 1/2 eq. 5 flux, reading A3; A12 for materials; LSERK4, A10):
@@ -191,6 +194,10 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 
 template <int MODE>
@@ -808,6 +815,21 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       }
     }
   };
+  // one slot: pull the next tile's TMA sources into L2 while this tile computes, so the TMA
+  // issued after the epilogue reads L2 rather than DRAM (cp.async.bulk.prefetch.L2)
+  auto prefetch_l2 = [&](int it) {
+    if (tid == 0) {
+      const int tile = tile_of(it);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) bulk_prefetch_l2(q + c * p.fstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3));
+      bulk_prefetch_l2(geo + (int64_t)tile * NG * TL, (unsigned)GB);
+      if (RES_TMA && MT::rk && read_res) {
+        const T* res = static_cast<const T*>(p.res);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) bulk_prefetch_l2(res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3));
+      }
+    }
+  };
   // cross-tile neighbour traces of tile `it` (same-tile ones are read from shared memory)
   auto issue_gather = [&](int it, const int32_t (&v)[KPT]) {
     if constexpr (MT::surf) {
@@ -866,6 +888,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       issue_gather(it + 1, vc1);
       cp_async_commit();
     }
+    if (S == 1 && it + 1 < n_it) prefetch_l2(it + 1);  // its TMA is issued after this tile
     if (it + 2 < n_it) load_codes(it + 2, vc2);
 
     const T* sq = sq_of(s);

@@ -29,6 +29,10 @@ if os.environ.get("TUNE_GRID") == "mma":  # only the fp64 tensor-core variants
     GRID = {8: [k for k in GRID[8] if k["M"] == 1]}
 if os.environ.get("TUNE_GRID") == "tf2":  # fp32 3xTF32 with the field-split team (4 warps)
     GRID = {4: [dict(R=8, S=s, C=c, M=2, Q=q) for s, c, q in itertools.product((1, 2), (2, 3, 4, 6), (0, 1))]}
+if os.environ.get("TUNE_GRID") == "all":  # every path: FMA, tensor-core (M=1), split teams (M=2)
+    GRID = {4: [dict(R=r, S=s, C=c, M=0, Q=0) for r, s, c in itertools.product((6, 8, 11), (1, 2), (3, 5))]
+            + [dict(R=8, S=s, C=c, M=1, Q=q) for s, c, q in itertools.product((1, 2), (3, 4, 6), (0, 1))]
+            + [dict(R=8, S=s, C=c, M=2, Q=q) for s, c, q in itertools.product((1, 2), (2, 3, 4), (0, 1))]}
 if os.environ.get("TUNE_GRID") == "m2":  # M=2 split teams (fp32 3xTF32 and fp64 DMMA), C>=1
     GRID = {4: [dict(R=8, S=s, C=c, M=2, Q=q) for s, c, q in itertools.product((1, 2), (1, 2, 3, 4), (0, 1))]}
 if os.environ.get("TUNE_GRID") == "tf":  # tensor-core variants (fp32 3xTF32, fp64 DMMA)
