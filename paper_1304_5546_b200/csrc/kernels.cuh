@@ -889,6 +889,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       cp_async_commit();
     }
     if (S == 1 && it + 1 < n_it) prefetch_l2(it + 1);  // its TMA is issued after this tile
+    if (S == 2 && it + 2 < n_it) prefetch_l2(it + 2);  // its TMA is issued at the next tile
     if (it + 2 < n_it) load_codes(it + 2, vc2);
 
     const T* sq = sq_of(s);
