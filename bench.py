@@ -283,9 +283,11 @@ def run_ours(args, rank, world, local_rank):
     launches = sum(v["launches"] for v in ctx.kernel_stats().values())
     kcfg = ctx.kernel_config()
     ctx.sync()
-    # per-launch kernel durations (roofline): a separate eagerly launched, event-bracketed pass
+    # per-launch kernel durations (roofline): a separate profiled pass -- the same graph replay with
+    # event-record nodes around every launch (dg_profile), read back between steps
+    prof_steps = min(args.steps, 20)
     ctx.profile(True)
-    ctx.run(dt, min(args.steps, 20))
+    ctx.run(dt, prof_steps)
     stats = ctx.kernel_stats()
     ctx.profile(False)
     ctx.sync()
@@ -307,7 +309,8 @@ def run_ours(args, rank, world, local_rank):
         """Roofline of one stage kernel: algorithmic bytes and flops per launch over its average
         event-timed launch.  The binding roof is HBM unless the arithmetic intensity exceeds the
         ridge of the pipe the contraction runs on (C5: N=8 fp64, 6.3 flop/B > 36 TF / 6.54 TB/s)."""
-        k_ms = stats[kind]["ms"] / max(stats[kind]["timed"], 1)
+        # per stage: a multi-rank fused stage is two launches (interior tiles, then boundary tiles)
+        k_ms = stats[kind]["ms"] / (5 * prof_steps)
         abytes = algorithmic_bytes_per_element_stage(Np, s, kind) * K_local
         flops = flops_per_element_stage(args.order, kind) * K_local
         achieved = abytes / (k_ms * 1e-3) / 1e9
@@ -321,6 +324,11 @@ def run_ours(args, rank, world, local_rank):
         main, alt = (cmp_roof, hbm_roof) if intensity > cpeak * 1e3 / hbm else (hbm_roof, cmp_roof)
         return dict(main, traffic=traffic_tab.get(f"N{args.order}_p{s}_n{args.n}_P{world}_{kind}"),
                     kernel=f"stage_kernel<{kind}>", algorithmic_bytes_per_launch=abytes, avg_launch_ms=k_ms,
+                    launches_per_stage=stats[kind]["timed"] / (5 * prof_steps),
+                    # the timed region itself holds only this kernel (fused variant, profiles/ launch list):
+                    # its CUDA-event time per stage, graph replay without the per-launch event nodes
+                    region_ms_per_stage=(ms / args.steps / 5) if kind == "fused" else None,
+                    region_frac=(abytes / (ms / args.steps / 5 * 1e-3) / 1e9 / hbm) if kind == "fused" else None,
                     flops_per_launch=flops, achieved_tflops=tflops, intensity_flop_per_byte=intensity,
                     ridge_flop_per_byte=cpeak * 1e3 / hbm,
                     other_roof={k: alt[k] for k in ("bound", "achieved", "peak", "unit", "frac", "peak_source")})

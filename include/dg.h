@@ -181,11 +181,15 @@ typedef struct {
 /* CUDA graphs for dg_run (single-rank contexts; default on): after one eager step, each
  * LSERK4 step (its 5 stage launches) is captured once per ping-pong parity for the current
  * dt and replayed with cudaGraphLaunch -- the same kernels and arguments, bitwise the same
- * result.  A new dt recaptures.  Profiling (dg_profile) runs eagerly.  0 disables (and
- * frees the graphs after synchronising the stream). */
+ * result.  A new dt recaptures.  While profiling (dg_profile) the replayed graph is a
+ * second capture with event-record nodes around every launch, and dg_run waits for each
+ * step to read them (between steps, outside every bracket).  0 disables (and frees the
+ * graphs after synchronising the stream). */
 dg_status dg_set_graphs(dg_ctx* c, int32_t enable);
 
-/* Turn per-launch CUDA-event timing on (1) or off (0); resets the statistics. */
+/* Turn per-launch CUDA-event timing on (1) or off (0); resets the statistics.  Eager
+ * launches are bracketed by events on the launching stream; graph replays by event-record
+ * nodes inside the graph (see dg_set_graphs). */
 dg_status dg_profile(dg_ctx* c, int32_t enable);
 
 /* Read the statistics (synchronises the stream when profiling is on). */

@@ -201,15 +201,20 @@ struct dg_ctx {
   cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
   ncclComm_t nccl_comm = nullptr;
   // CUDA graphs: one LSERK4 step (5 stages) per graph, one per starting ping-pong parity,
-  // captured for the current dt (single-rank contexts; eager while profiling)
+  // captured for the current dt (single-rank contexts).  While profiling, a second pair of
+  // graphs carries event-record nodes around every launch (pexec/pev below).
   bool graphs = true;
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  cudaGraphExec_t pexec[2] = {nullptr, nullptr};
   double gdt = 0.0;
   // profiling
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
   struct Timed { int kind; int ev0, ev1; };
   std::vector<Timed> timed;
+  int pcap = -1;                        // parity of the profiled graph being captured, else -1
+  std::vector<cudaEvent_t> pev[2];      // event-record nodes of profiled graph [parity]
+  std::vector<Timed> ptimed[2];         // (kind, event pair) per launch of that graph
   dg_kernel_stats stats{};
 };
 
@@ -246,6 +251,17 @@ int take_event(dg_ctx* c) {
 }
 
 dg_status launch_stage(dg_ctx* c, int mode, const dg::StageArgs& a, cudaStream_t s, int kind) {
+  if (c->pcap >= 0) {  // capturing a profiled graph: external event-record nodes bracket the launch
+    std::vector<cudaEvent_t>& pe = c->pev[c->pcap];  // created before the capture began
+    const int ev = 2 * (int)c->ptimed[c->pcap].size();
+    if (ev + 2 > (int)pe.size()) return set_err(DG_E_STATE, "profiled graph: event pool exhausted");
+    CU(c, cudaEventRecordWithFlags(pe[ev], s, cudaEventRecordExternal));
+    cudaError_t e = c->km->launch(mode, c->material, a, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "stage kernel launch");
+    CU(c, cudaEventRecordWithFlags(pe[ev + 1], s, cudaEventRecordExternal));
+    c->ptimed[c->pcap].push_back({kind, ev, ev + 1});
+    return DG_OK;
+  }
   int ev = -1;
   if (c->profiling) {
     ev = take_event(c);
@@ -701,18 +717,33 @@ dg_status dg_get_fields(dg_ctx* c, double* Hx, double* Hy, double* Ez) {
 }
 
 static void drop_graphs(dg_ctx* c) {
-  for (auto& g : c->gexec)
-    if (g) {
-      cudaGraphExecDestroy(g);
-      g = nullptr;
-    }
+  for (int p = 0; p < 2; ++p) {
+    for (cudaGraphExec_t* g : {&c->gexec[p], &c->pexec[p]})
+      if (*g) {
+        cudaGraphExecDestroy(*g);
+        *g = nullptr;
+      }
+    for (cudaEvent_t e : c->pev[p]) cudaEventDestroy(e);
+    c->pev[p].clear();
+    c->ptimed[p].clear();
+  }
 }
 
-// Capture one LSERK4 step starting from q[parity] (the same launches run_stage enqueues)
-static dg_status capture_step(dg_ctx* c, double dt, int parity) {
+// Capture one LSERK4 step starting from q[parity] (the same launches run_stage enqueues);
+// profiled = with event-record nodes around every launch (into pexec[parity])
+static dg_status capture_step(dg_ctx* c, double dt, int parity, bool profiled = false) {
   const int cur0 = c->cur;
   const dg_kernel_stats st0 = c->stats;
   c->cur = parity;
+  c->pcap = profiled ? parity : -1;
+  if (profiled) {  // two launches per stage at most (split variant): 20 events
+    c->ptimed[parity].clear();
+    while (c->pev[parity].size() < 20) {
+      cudaEvent_t ev;
+      CU(c, cudaEventCreate(&ev));
+      c->pev[parity].push_back(ev);
+    }
+  }
   CU(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   dg_status st = DG_OK;
   for (int i = 0; i < 5 && st == DG_OK; ++i) st = run_stage(c, i, dt);
@@ -720,12 +751,13 @@ static dg_status capture_step(dg_ctx* c, double dt, int parity) {
   const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
   c->cur = cur0;
   c->stats = st0;
+  c->pcap = -1;
   if (st != DG_OK) {
     if (g) cudaGraphDestroy(g);
     return st;
   }
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamEndCapture");
-  const cudaError_t e2 = cudaGraphInstantiate(&c->gexec[parity], g, 0);
+  const cudaError_t e2 = cudaGraphInstantiate(profiled ? &c->pexec[parity] : &c->gexec[parity], g, 0);
   cudaGraphDestroy(g);
   if (e2 != cudaSuccess) return cuda_fail(c, e2, "cudaGraphInstantiate");
   return DG_OK;
@@ -739,13 +771,28 @@ dg_status dg_run(dg_ctx* c, double dt, int64_t nsteps) {
   CU(c, cudaSetDevice(c->device));
   for (int64_t s = 0; s < nsteps; ++s) {
     // graph replay once a step has run eagerly (kernel attributes set up outside any capture)
-    if (c->graphs && c->nranks == 1 && !c->profiling && c->steps_done > 0) {
+    if (c->graphs && c->nranks == 1 && c->steps_done > 0) {
       if (c->gdt != dt) {
         drop_graphs(c);
         c->gdt = dt;
       }
-      if (!c->gexec[c->cur] && (st = capture_step(c, dt, c->cur)) != DG_OK) return st;
-      CU(c, cudaGraphLaunch(c->gexec[c->cur], c->stream));
+      const int par = c->cur;
+      if (!c->profiling) {
+        if (!c->gexec[par] && (st = capture_step(c, dt, par)) != DG_OK) return st;
+        CU(c, cudaGraphLaunch(c->gexec[par], c->stream));
+      } else {
+        // profiled replay: the same launches with event-record nodes; the per-launch times
+        // are read back after each step (the host wait lies between steps, outside every bracket)
+        if (!c->pexec[par] && (st = capture_step(c, dt, par, true)) != DG_OK) return st;
+        CU(c, cudaGraphLaunch(c->pexec[par], c->stream));
+        CU(c, cudaStreamSynchronize(c->stream));
+        for (const auto& t : c->ptimed[par]) {
+          float ms = 0.f;
+          CU(c, cudaEventElapsedTime(&ms, c->pev[par][t.ev0], c->pev[par][t.ev1]));
+          c->stats.ms[t.kind] += ms;
+          c->stats.timed[t.kind] += 1;
+        }
+      }
       c->stats.launches[c->fused ? 0 : 1] += 5;
       if (!c->fused) c->stats.launches[2] += 5;
       c->cur = 1 - c->cur;  // five stages: five ping-pong flips

@@ -57,3 +57,28 @@ def test_graphs_toggle_midrun():
     for other in res[1:]:
         for a, b in zip(res[0], other):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_profiled_graph_replay(fused):
+    """dg_profile with graphs on: the replayed graph carries event-record nodes around every
+    launch; same fields bitwise as the unprofiled replay, every launch timed, times > 0."""
+    VX, VY, E = dginputs.rect_mesh(12)
+    outs = []
+    for prof in (False, True):
+        c = dg.dg_setup(5, VX, VY, E, precision=4, fused=fused)
+        x, y = c.nodes()
+        c.set_fields(*dginputs.cavity_mode(x, y, 0.0))
+        c.run(1e-3, 2)
+        c.profile(prof)
+        c.run(1e-3, 5)  # both parities
+        st = c.kernel_stats()
+        outs.append(c.get_fields())
+        c.destroy()
+        if prof:
+            kinds = ("fused",) if fused else ("volume", "surface")
+            for k in kinds:
+                assert st[k]["launches"] == 25 and st[k]["timed"] == 25, st
+                assert st[k]["ms"] > 0
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
