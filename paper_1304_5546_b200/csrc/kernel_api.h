@@ -74,9 +74,20 @@ struct KernelModule {
   KernelInfo (*info)() = nullptr;
   bool (*check_fmask)(const int* Fmask) = nullptr;
   // column swizzle of the tile-blocked layout: element `lane` of node row n lives at
-  // column lane ^ (swizzle * (n & 3)) (0 = plain layout)
+  // column swz_col(swizzle, n, lane) (0 = plain layout)
   int swizzle = 0;
 };
+
+// Column of element e (0..31) of node row n in the tile-blocked layout, swizzle mode swm:
+// e ^ (swm * s(n)).  s(n) = n & 3 for the DMMA layout (swm = 4: B-fragment loads of rows
+// 4k..4k+3 conflict free); for the 3xTF32 layout (swm = 8) s(n) = (n & 3) ^ ((n >> 2) & 1),
+// which keeps both of its fragment patterns bank-conflict free: A fragments read rows
+// 4j + {0..3} (s = 4 distinct values for every j), C fragments rows 8t + 2i + h, i = 0..3
+// (s(h), s(2+h), s(4+h), s(6+h) distinct).  An XOR of a multiple of 8 keeps 8-element groups
+// contiguous, so global accesses stay 32 B-sector aligned.  The map is its own inverse.
+__host__ __device__ constexpr int swz_col(int swm, int n, int e) {
+  return e ^ (swm * (swm == 8 ? ((n & 3) ^ ((n >> 2) & 1)) : (n & 3)));
+}
 
 // Registry: one entry per compiled (N, prec); nullptr if not compiled.
 const KernelModule* find_module(int N, int prec);

@@ -112,12 +112,25 @@ constexpr size_t DVB = USE_TF ? (size_t)KVT * NT * 32 * 32
 constexpr size_t LVB = USE_TF ? (size_t)KLT * NT * 32 * 16
                               : USE_MMA ? (size_t)KL * PR * 32 * 8 : (size_t)NFC * RPL * VC * sizeof(T);
 constexpr size_t OPB = ((DVB + LVB + 15) / 16) * 16;
+// DG_OG (tensor-core paths): the per-lane operator fragments are read from global memory
+// through L1 (ld.global.nc) instead of a shared-memory copy per CTA, freeing OPB bytes of
+// shared memory per team (more resident teams); every resident team shares the L1 copy
+#ifndef DG_OG
+#define DG_OG 0
+#endif
+constexpr bool OPS_GLOBAL = DG_OG && (DG_MMA != 0);
+constexpr size_t OPB_SMEM = OPS_GLOBAL ? 0 : OPB;
+template <typename V>
+__device__ __forceinline__ V ldop(const V* p) {
+  if constexpr (OPS_GLOBAL) return __ldg(p);
+  else return *p;
+}
 // Column swizzle of the tile-blocked layout: element e of node row n is stored at
-// column e ^ (SWM * (n & 3)).  Identity for the FMA kernels; for the DMMA kernels
+// column swz_col(SWM, n, e) (kernel_api.h).  Identity for the FMA kernels; for the DMMA kernels
 // it makes the B-fragment loads (4 rows x 8 elements) bank-conflict free, for the
 // TF32 kernels the A-fragment loads (8 elements x 4 nodes).
 constexpr int SWM = USE_MMA ? 4 : (USE_TF ? 8 : 0);
-__host__ __device__ constexpr int colx(int n, int e) { return e ^ (SWM * (n & 3)); }
+__host__ __device__ constexpr int colx(int n, int e) { return dg::swz_col(SWM, n, e); }
 constexpr size_t QB = (size_t)3 * NP * TL * sizeof(T);
 __host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)(mat ? dg::NGEO_MAT : dg::NGEO_CONST) * TL * sizeof(T); }
 constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
@@ -127,12 +140,19 @@ constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
 #define DG_RT 1
 #endif
 constexpr bool RES_TMA = USE_TF && DG_RT;
+// DG_FF: phase order of the fused kernels.  0: volume -> flux -> LIFT (the volume
+// accumulators stay live across the flux phase); 1: flux -> volume -> LIFT (nothing but the
+// face-point codes is live during the flux phase, so the peak register count drops)
+#ifndef DG_FF
+#define DG_FF 0
+#endif
+constexpr bool FLUX_FIRST = DG_FF;
 __host__ __device__ constexpr size_t slot_bytes(bool surf, bool mat, bool rk) {
   return QB + geo_bytes(mat) + (surf ? SPB : 0) + (RES_TMA && rk ? QB : 0);
 }
 constexpr size_t BARB = 64;  // mbarriers: one per slot
 __host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat, bool rk) {
-  return BARB + OPB + S * slot_bytes(surf, mat, rk);
+  return BARB + OPB_SMEM + S * slot_bytes(surf, mat, rk);
 }
 // Slots per team: 2 = double-buffered (tile t+1 streams in while t computes), 1 = latency
 // hidden across resident teams instead.  Measured at C4 (N=5): fp32 is issue-bound and
@@ -146,7 +166,16 @@ constexpr int CTAS_BY_SMEM = (int)((227 * 1024) / smem_total(nslots(true, false)
 #define DG_C 5  // measured (C4 fp32): 5 teams x 128 registers beats 8 x 80 (spills) and 4 x 168
 #endif
 constexpr int MIN_CTAS = CTAS_BY_SMEM < 1 ? 1 : (CTAS_BY_SMEM > DG_C ? DG_C : CTAS_BY_SMEM);
-constexpr int KPT = (NF + P - 1) / P;  // face points per thread (point m belongs to warp m % P)
+// Face points per thread.  Face-major (when P divides Nfp): warp g owns points i = g + jP of
+// every face f, k = f KPF + j, so each face's nx, ny, Fsc, Bsc are loaded once per warp;
+// otherwise point m = g + kP (balanced when P does not divide Nfp).
+constexpr bool FACE_MAJOR = NFP % P == 0;
+constexpr int KPF = (NFP + P - 1) / P;
+constexpr int KPT = FACE_MAJOR ? 3 * KPF : (NF + P - 1) / P;
+__device__ __forceinline__ int point_of(int g, int k) {  // face point of slot k of warp g, NF if none
+  if constexpr (FACE_MAJOR) return (k / KPF) * NFP + g + (k % KPF) * P;
+  else return g + k * P < NF ? g + k * P : NF;
+}
 
 // Face node ids, increasing node index (closed form of the node ordering: row j
 // of the triangle starts at j(N+1) - j(j-1)/2).  Checked against the setup's
@@ -263,7 +292,7 @@ __device__ __forceinline__ void volume_rows(const T* __restrict__ sq, const DVT*
 }
 
 // ---------------------------------------------------------------- phase B: flux
-// Face points m = g, g+P, ... of this thread's element; the Fsc-scaled flux
+// Face points point_of(g, k) of this thread's element; the Fsc-scaled flux
 // (the vector f^k of eq. 8) overwrites the neighbour trace q+ in place.
 // Neighbour index codes (vmapP, runtime.cu): >= 0 an offset into a field in
 // global memory (gathered into sp); < 0 a neighbour in the SAME tile, read
@@ -273,9 +302,9 @@ __device__ __forceinline__ void flux_points(const T* __restrict__ sq, const T* _
                                             const int32_t (&vmc)[KPT], int g, int lane, T alpha) {
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
-    const int m = g + k * P;
+    const int m = point_of(g, k);
     if (m >= NF) break;
-    const int f = m < NFP ? 0 : (m < 2 * NFP ? 1 : 2);
+    const int f = FACE_MAJOR ? k / KPF : (m < NFP ? 0 : (m < 2 * NFP ? 1 : 2));  // compile-time if face-major
     const int i = m - f * NFP;
     const int fm = f == 0 ? i : (f == 1 ? row_start(i) + N - i : row_start(i));
     const T nx = gg[(4 + 3 * f) * TL], ny = gg[(5 + 3 * f) * TL], hF = gg[(6 + 3 * f) * TL];
@@ -343,7 +372,7 @@ __device__ __forceinline__ void volume_mma(const double* __restrict__ sq, const 
   for (int ks = 0; ks < KV; ++ks) {
     const int j = 4 * ks + (lane & 3);
     const int jc = j < NP ? j : NP - 1;  // padded k rows: A is zero there
-    const AVT a = AV[(ks * PR + g) * 32 + lane];
+    const AVT a = ldop(AV + (ks * PR + g) * 32 + lane);
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int addr = jc * TL + colx(jc, 8 * nt + (lane >> 2));
@@ -374,7 +403,7 @@ __device__ __forceinline__ void lift_mma(const double* __restrict__ sp, const do
   for (int ks = 0; ks < KL; ++ks) {
     const int m = 4 * ks + (lane & 3);
     const int mc = m < NF ? m : NF - 1;
-    const double a = AL[(ks * PR + g) * 32 + lane];
+    const double a = ldop(AL + (ks * PR + g) * 32 + lane);
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int addr = mc * TL + colx(mc, 8 * nt + (lane >> 2));
@@ -431,10 +460,15 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
   const int tig = lane & 3;
   const int ee[2] = {16 * mt + (lane >> 2), 16 * mt + (lane >> 2) + 8};
   // Lane-invariant shared-memory offsets.  A fragments read node rows 8ks + 4kh + tig, whose
-  // swizzle (row & 3 = tig) does not depend on (ks, kh): row offsets are compile-time.  Rows
-  // past Np / 3Nfp meet zero B rows; they read the next field, the geometry block (fields) or
-  // zeroed pad rows (flux), all finite.  C fragments: row 8nt + 2tig + h, element ee[i].
-  const int abase[2] = {tig * TL + (ee[0] ^ (8 * tig)), tig * TL + (ee[1] ^ (8 * tig))};
+  // swizzle (swz_col: s = tig ^ kh) depends only on kh (compile-time per register): row offsets
+  // are compile-time.  Rows past Np / 3Nfp meet zero B rows; they read the next field, the
+  // geometry block (fields) or zeroed pad rows (flux), all finite.  C fragments: row
+  // 8nt + 2tig + h, element ee[i].
+  int abase[2][2];  // [kh][i]
+#pragma unroll
+  for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) abase[kh][i] = tig * TL + colx(4 * kh + tig, ee[i]);
   int cbase[4];  // C register r -> row (2tig + (r & 1)) offset + swizzled column of ee[r >> 1]
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -443,6 +477,10 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
   }
   auto row_ok = [&](int nt, int r) { return NT * 8 == NP || nt < NT - 1 || 8 * nt + 2 * tig + (r & 1) < NP; };
   const int64_t tbase = (int64_t)tile * NP * TL;
+  if constexpr (FLUX_FIRST && MT::surf) {
+    flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
+    __syncthreads();
+  }
   TT acc[NFLD][NT][4];  // acc[f]: field F0 + f
   if constexpr (MT::vol) {
     TT rxe[2], sxe[2], rye[2], sye[2];
@@ -467,7 +505,7 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
 #pragma unroll
       for (int r = 0; r < 4; ++r) {  // A register r: element ee[r & 1], node 8ks + tig + 4(r >> 1)
         const int i = r & 1;
-        const TT* a = sq + abase[i] + (8 * ks + 4 * (r >> 1)) * TL;
+        const TT* a = sq + abase[r >> 1][i] + (8 * ks + 4 * (r >> 1)) * TL;
         if constexpr (UV) split_tf32(a[2 * NP * TL], ezh[r], ezl[r]);
         if constexpr (WW) {
           const TT hx = a[0], hy = a[NP * TL];
@@ -477,8 +515,8 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const float4 bh = BV[(ks * NT + nt) * 64];  // hi and lo: 32 lanes x 16 B contiguous each
-        const float4 bl = BV[(ks * NT + nt) * 64 + 32];
+        const float4 bh = ldop(BV + (ks * NT + nt) * 64);  // hi and lo: 32 lanes x 16 B contiguous each
+        const float4 bl = ldop(BV + (ks * NT + nt) * 64 + 32);
         if constexpr (UV) {
           tmma3(acc[0][nt], ezh, ezl, bh.x, bh.y, bl.x, bl.y);
           tmma3(acc[1][nt], ezh, ezl, bh.z, bh.w, bl.z, bl.w);
@@ -532,21 +570,23 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
     }
   }
   if constexpr (MT::surf) {
-    flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
-    __syncthreads();
+    if constexpr (!FLUX_FIRST) {
+      flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
+      __syncthreads();
+    }
     const float4* BL = reinterpret_cast<const float4*>(ops + DVB) + lane;
 #pragma unroll
     for (int ks = 0; ks < KLT; ++ks) {
       uint32_t fh[NFLD][4], fl[NFLD][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const TT* a = sp + abase[r & 1] + (8 * ks + 4 * (r >> 1)) * TL;
+        const TT* a = sp + abase[r >> 1][r & 1] + (8 * ks + 4 * (r >> 1)) * TL;
 #pragma unroll
         for (int f = 0; f < NFLD; ++f) split_tf32(a[(F0 + f) * NFE * TL], fh[f][r], fl[f][r]);
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const float4 b = BL[(ks * NT + nt) * 32];
+        const float4 b = ldop(BL + (ks * NT + nt) * 32);
 #pragma unroll
         for (int f = 0; f < NFLD; ++f) tmma3(acc[f][nt], fh[f], fl[f], b.x, b.y, b.z, b.w);
       }
@@ -645,6 +685,10 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
   constexpr bool ACT[3] = {FS != 2, FS != 2, FS != 1};  // output fields of this warp
   const int n = 8 * rg + (lane >> 2);  // this lane's output row
   const int nc = n < NP ? n : NP - 1;
+  if constexpr (FLUX_FIRST && MT::surf) {
+    flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
+    __syncthreads();
+  }
   TT rhx[4][2], rhy[4][2], rez[4][2];
   if constexpr (MT::vol) {
     TT u[4][2], v[4][2];
@@ -691,8 +735,10 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
     }
   }
   if constexpr (MT::surf) {
-    flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
-    __syncthreads();
+    if constexpr (!FLUX_FIRST) {
+      flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
+      __syncthreads();
+    }
     lift_mma<FS>(sp, reinterpret_cast<const TT*>(ops + DVB), rg, lane, rhx, rhy, rez);
   }
   if constexpr (MAT) {
@@ -771,7 +817,8 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [0, S): slots, [S]: residual
   const DV_t* DV = reinterpret_cast<const DV_t*>(smem_raw + BARB);
   const LV_t* LV = reinterpret_cast<const LV_t*>(smem_raw + BARB + DVB);
-  unsigned char* slots = smem_raw + BARB + OPB;
+  unsigned char* slots = smem_raw + BARB + OPB_SMEM;
+  const unsigned char* opsrc = OPS_GLOBAL ? static_cast<const unsigned char*>(p.ops) : smem_raw + BARB;
   auto sq_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT); };
   auto sg_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB); };
   auto sp_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB + GB); };
@@ -789,7 +836,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       const int32_t* src = p.vmapP + (int64_t)tile_of(it) * NF * TL + lane;
 #pragma unroll
       for (int k = 0; k < KPT; ++k) {
-        const int m = g + k * P;
+        const int m = point_of(g, k);
         v[k] = m < NF ? __ldg(src + m * TL) : -1;
       }
     }
@@ -836,7 +883,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       T* sp = sp_of(it % S) + lane;
 #pragma unroll
       for (int k = 0; k < KPT; ++k) {
-        const int m = g + k * P;
+        const int m = point_of(g, k);
         if (m < NF && v[k] >= 0) {
           const T* src = q + v[k];
           T* dst = sp - lane + m * TL + colx(m, lane);
@@ -855,7 +902,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   {
     const int4* src = reinterpret_cast<const int4*>(p.ops);
     int4* dst = reinterpret_cast<int4*>(smem_raw + BARB);
-    for (int i = tid; i < (int)(OPB / 16); i += TEAM) cp_async16(dst + i, src + i);
+    for (int i = tid; i < (int)(OPB_SMEM / 16); i += TEAM) cp_async16(dst + i, src + i);
     if constexpr (MT::surf && NFE > NF) {
       constexpr int PADN = (NFE - NF) * TL;
       for (int i = tid; i < S * 3 * PADN; i += TEAM) {
@@ -898,22 +945,26 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     if constexpr (USE_MMA) {
       if constexpr (DMMA_SPLIT) {
         if (g < PR)
-          mma_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, g, lane, alpha, read_res);
+          mma_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, opsrc, vc0, tile, g, g, lane, alpha, read_res);
         else
-          mma_tile<MODE, MAT, 2>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, g - PR, lane, alpha, read_res);
+          mma_tile<MODE, MAT, 2>(p, sq, sg_of(s), sp, opsrc, vc0, tile, g, g - PR, lane, alpha, read_res);
       } else {
-        mma_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, smem_raw + BARB, vc0, tile, g, g, lane, alpha, read_res);
+        mma_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, opsrc, vc0, tile, g, g, lane, alpha, read_res);
       }
     } else if constexpr (USE_TF) {
       if constexpr (TF_SPLIT) {
         if (g < 2)
-          tf_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, sr_of(s), smem_raw + BARB, vc0, tile, g, g & 1, lane, alpha, read_res);
+          tf_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, g & 1, lane, alpha, read_res);
         else
-          tf_tile<MODE, MAT, 2>(p, sq, sg_of(s), sp, sr_of(s), smem_raw + BARB, vc0, tile, g, g & 1, lane, alpha, read_res);
+          tf_tile<MODE, MAT, 2>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, g & 1, lane, alpha, read_res);
       } else {
-        tf_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, sr_of(s), smem_raw + BARB, vc0, tile, g, g, lane, alpha, read_res);
+        tf_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, g, lane, alpha, read_res);
       }
     } else {
+    if constexpr (FLUX_FIRST && MT::surf) {
+      flux_points<MAT>(sq, gg, sp, vc0, g, lane, alpha);
+      __syncthreads();
+    }
     T rhx[R], rhy[R], rez[R];
     if constexpr (MT::vol) {
       volume_rows(sq, DV, n0, lane, gg[0 * TL], gg[1 * TL], gg[2 * TL], gg[3 * TL], rhx, rhy, rez);
@@ -945,8 +996,10 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       }
     }
     if constexpr (MT::surf) {
-      flux_points<MAT>(sq, gg, sp, vc0, g, lane, alpha);
-      __syncthreads();
+      if constexpr (!FLUX_FIRST) {
+        flux_points<MAT>(sq, gg, sp, vc0, g, lane, alpha);
+        __syncthreads();
+      }
       lift_rows(sp, LV, n0, lane, rhx, rhy, rez);
     }
     // material factors 1/mu, 1/eps (reading A12).  In split mode the volume kernel

@@ -97,7 +97,7 @@ Nccl* nccl() {
 // canonical fp64 [3][Kl][Np]  <->  tile-blocked T [3][fstride].  Device slot d
 // (tile d/32, lane d%32) holds local element perm[d] (-1: padding);
 // slot_of[kl] is the inverse.
-// (column swizzle swm: element `lane` of node row n sits at column lane ^ (swm * (n & 3)))
+// (column swizzle swm: element `lane` of node row n sits at column dg::swz_col(swm, n, lane))
 template <typename T>
 __global__ void to_blocked(const double* __restrict__ src, T* __restrict__ q, const int32_t* __restrict__ perm,
                            int64_t Kl, int64_t Kpad, int Np, int64_t fstride, int swm) {
@@ -108,7 +108,7 @@ __global__ void to_blocked(const double* __restrict__ src, T* __restrict__ q, co
     const int64_t tn = o >> 5;
     const int64_t t = tn / Np;
     const int n = (int)(tn - t * Np);
-    const int lane = (int)(o & 31) ^ (swm * (n & 3));
+    const int lane = dg::swz_col(swm, n, (int)(o & 31));
     const int64_t kl = perm[t * 32 + lane];
     q[c * fstride + o] = (kl >= 0) ? static_cast<T>(src[(c * Kl + kl) * Np + n]) : T(0);
   }
@@ -125,7 +125,7 @@ __global__ void from_blocked(const T* __restrict__ q, double* __restrict__ dst, 
     const int n = (int)(o - kl * Np);
     const int64_t d = slot_of[kl];
     dst[c * total + o] =
-        static_cast<double>(q[c * fstride + ((d >> 5) * Np + n) * 32 + ((d & 31) ^ (swm * (n & 3)))]);
+        static_cast<double>(q[c * fstride + ((d >> 5) * Np + n) * 32 + dg::swz_col(swm, n, (int)(d & 31))]);
   }
 }
 
@@ -389,7 +389,7 @@ void upload_geometry(dg_ctx* c, std::vector<T>& g, std::vector<int32_t>& vp, con
   vp.assign((size_t)c->ntiles * NF * 32, 0);
   const int swm = c->km->swizzle;
   // blocked (column-swizzled) offset of node n of the element in device slot d
-  auto col = [&](int64_t d, int n) -> int64_t { return (d & 31) ^ (swm * (n & 3)); };
+  auto col = [&](int64_t d, int n) -> int64_t { return dg::swz_col(swm, n, (int)(d & 31)); };
   auto blk = [&](int64_t d, int n) -> int64_t { return ((d >> 5) * Np + n) * 32 + col(d, n); };
   // neighbour node n of the element in slot d2, seen from slot d: same tile -> shared-memory
   // offset within the tile's field block, encoded negative: -(1 + n*32 + column)
@@ -536,7 +536,7 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
       const int64_t gd = c->mesh.send_gdof[s];
       const int64_t k = gd / Np, n = gd - (gd / Np) * Np;
       const int64_t d = c->slot_of[c->mesh.g2l[k]];
-      si[s] = (int32_t)(((d >> 5) * Np + n) * 32 + ((d & 31) ^ (c->km->swizzle * (n & 3))));
+      si[s] = (int32_t)(((d >> 5) * Np + n) * 32 + dg::swz_col(c->km->swizzle, (int)n, (int)(d & 31)));
     }
     if ((st = alloc(c, (void**)&c->send_idx, si.size() * sizeof(int32_t))) != DG_OK) return st;
     CU(c, cudaMemcpy(c->send_idx, si.data(), si.size() * sizeof(int32_t), cudaMemcpyHostToDevice));

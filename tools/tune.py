@@ -18,7 +18,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-VDIR = os.path.join(ROOT, "build_variants")
+VDIR = os.path.join(ROOT, os.environ.get("TUNE_VDIR", "build_variants"))
 
 GRID = {
     4: [dict(R=r, S=s, C=c, M=0) for r, s, c in itertools.product((6, 8, 11), (1, 2), (3, 5))],
@@ -35,12 +35,23 @@ if os.environ.get("TUNE_GRID") == "all":  # every path: FMA, tensor-core (M=1), 
             + [dict(R=8, S=s, C=c, M=2, Q=q) for s, c, q in itertools.product((1, 2), (2, 3, 4), (0, 1))]}
 if os.environ.get("TUNE_GRID") == "m2":  # M=2 split teams (fp32 3xTF32 and fp64 DMMA), C>=1
     GRID = {4: [dict(R=8, S=s, C=c, M=2, Q=q) for s, c, q in itertools.product((1, 2), (1, 2, 3, 4), (0, 1))]}
+if os.environ.get("TUNE_GRID") == "ff":  # flux-first phase order, every path, C up to 8
+    GRID = {4: [dict(R=r, S=s, C=c, M=0, Q=0, F=1) for r, s, c in itertools.product((6, 8), (1, 2), (3, 5, 6))]
+            + [dict(R=8, S=s, C=c, M=1, Q=q, F=1) for s, c, q in itertools.product((1, 2), (3, 4, 5, 6, 8), (0, 1))]
+            + [dict(R=8, S=s, C=c, M=2, Q=1, F=1) for s, c in itertools.product((1, 2), (2, 3, 4))]}
+if os.environ.get("TUNE_GRID") == "ff":  # + the current picks (volume first) for a same-box comparison
+    _cur = json.load(open(os.path.join(ROOT, "paper_1304_5546_b200", "csrc", "tune.json")))
+    GRID[0] = [dict(R=v["R"], S=v["S"], C=v["C"], M=v["M"], Q=v["Q"], F=0) for k, v in _cur.items()
+               if not k.startswith("_")]
+if os.environ.get("TUNE_GRID") == "og":  # tensor-core paths, flux first, operators via L1 (G=1)
+    GRID = {4: [dict(R=8, S=s, C=c, M=m, Q=1, F=1, G=1) for s, c, m in itertools.product((1, 2), (4, 5, 6, 8), (1, 2))]}
 if os.environ.get("TUNE_GRID") == "tf":  # tensor-core variants (fp32 3xTF32, fp64 DMMA)
     GRID = {4: [dict(R=8, S=s, C=c, M=1, Q=q) for s, c, q in itertools.product((1, 2), (3, 4, 6), (0, 1))]}
 
 
 def name_of(k):
-    return f"R{k['R']}_S{k['S']}_C{k['C']}_M{k['M']}" + (f"_Q{k['Q']}" if "Q" in k else "")
+    return (f"R{k['R']}_S{k['S']}_C{k['C']}_M{k['M']}" + (f"_Q{k['Q']}" if "Q" in k else "")
+            + (f"_F{k['F']}" if "F" in k else "") + (f"_G{k['G']}" if "G" in k else ""))
 
 
 def cmd_build():
@@ -134,7 +145,10 @@ def cmd_pick(*paths):
         kn = {x[0]: int(x[1:]) for x in parts}
         kn.setdefault("M", 0)
         kn.setdefault("Q", 0)  # sweeps before the knob existed: register prefetch
-        tune[key] = dict(R=kn["R"], S=kn["S"], C=kn["C"], M=kn["M"], Q=kn["Q"], ms=round(r["ms"], 5))
+        kn.setdefault("F", 0)  # sweeps before the knob existed: volume first
+        kn.setdefault("G", 0)  # sweeps before the knob existed: operators in shared memory
+        tune[key] = dict(R=kn["R"], S=kn["S"], C=kn["C"], M=kn["M"], Q=kn["Q"], F=kn["F"], G=kn["G"],
+                         ms=round(r["ms"], 5))
     out = os.path.join(ROOT, "paper_1304_5546_b200", "csrc", "tune.json")
     with open(out, "w") as fh:
         json.dump(tune, fh, indent=1)
