@@ -206,7 +206,9 @@ typedef struct {
   int32_t slots;         /* shared-memory pipeline slots (1 or 2) */
   int32_t residual_tma;  /* 1: the LSERK4 residual is staged into shared memory by TMA */
   int32_t teams_cap;     /* cap on resident CTAs per SM (launch bounds) */
-  int32_t reserved;
+  int32_t flags;         /* bit 0: flux phase before the volume phase (knob F);
+                            bit 1: tensor-core operator fragments read through L1 from global
+                            memory instead of a shared-memory copy per CTA (knob G) */
   int64_t smem_bytes;    /* dynamic shared memory per CTA of the fused stage kernel */
 } dg_kernel_config;
 dg_status dg_get_kernel_config(const dg_ctx* c, dg_kernel_config* out);

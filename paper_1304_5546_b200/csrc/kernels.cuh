@@ -1204,6 +1204,7 @@ dg::KernelInfo info() {
   k.contraction = USE_TF ? 2 : (USE_MMA ? 1 : 0);
   k.residual_tma = RES_TMA ? 1 : 0;
   k.teams_cap = DG_C;
+  k.flags = (FLUX_FIRST ? 1 : 0) | (OPS_GLOBAL ? 2 : 0);
   return k;
 }
 

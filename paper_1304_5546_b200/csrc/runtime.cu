@@ -1077,7 +1077,7 @@ dg_status dg_get_kernel_config(const dg_ctx* c, dg_kernel_config* out) {
   out->slots = k.slots;
   out->residual_tma = k.residual_tma;
   out->teams_cap = k.teams_cap;
-  out->reserved = 0;
+  out->flags = k.flags;
   out->smem_bytes = (int64_t)k.smem_bytes;
   return DG_OK;
 }

@@ -59,7 +59,7 @@ KIND = ("fused", "volume", "surface", "helper")
 
 class KernelConfig(C.Structure):
     _fields_ = [("contraction", C.c_int32), ("threads", C.c_int32), ("slots", C.c_int32),
-                ("residual_tma", C.c_int32), ("teams_cap", C.c_int32), ("reserved", C.c_int32),
+                ("residual_tma", C.c_int32), ("teams_cap", C.c_int32), ("flags", C.c_int32),
                 ("smem_bytes", C.c_int64)]
 
 
@@ -279,7 +279,8 @@ class Context:
         k = KernelConfig()
         _check(_lib.dg_get_kernel_config(self._h, C.byref(k)))
         return dict(contraction=CONTRACTION[k.contraction], threads=k.threads, slots=k.slots,
-                    residual_tma=bool(k.residual_tma), teams_cap=k.teams_cap, smem_bytes=k.smem_bytes)
+                    residual_tma=bool(k.residual_tma), teams_cap=k.teams_cap, smem_bytes=k.smem_bytes,
+                    flux_first=bool(k.flags & 1), ops_global=bool(k.flags & 2))
 
     def kernel_stats(self):
         st = KernelStats()

@@ -24,7 +24,7 @@ def launches(path):
     for r in rows[2:]:
         d = dict(zip(hdr, r))
         b = sum(float(d[k]) * SCALE[units[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        res.append(b)
+        res.append((d.get("Kernel Name", ""), b))
     return res
 
 
@@ -37,9 +37,15 @@ def main():
                    "bench.py for roofline.traffic.")
     for arg in sys.argv[1:]:
         key, path = arg.split("=", 1)
-        b = launches(path)
-        tab[key] = sum(b) / len(b)
-        print(key, len(b), "launches", [f"{x / 1e9:.3f}" for x in b], f"mean {tab[key] / 1e9:.4f} GB")
+        ls = launches(path)
+        if key.endswith("_split"):  # a split-variant capture: volume = stage_kernel<1, .>, surface = <2, .>
+            groups = {key[:-6] + "_volume": [b for n, b in ls if "stage_kernel<1" in n.replace("(int)", "")],
+                      key[:-6] + "_surface": [b for n, b in ls if "stage_kernel<2" in n.replace("(int)", "")]}
+        else:
+            groups = {key: [b for _, b in ls]}
+        for k, b in groups.items():
+            tab[k] = sum(b) / len(b)
+            print(k, len(b), "launches", [f"{x / 1e9:.3f}" for x in b], f"mean {tab[k] / 1e9:.4f} GB")
     with open(out, "w") as fh:
         json.dump(tab, fh, indent=1)
 

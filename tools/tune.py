@@ -44,7 +44,10 @@ if os.environ.get("TUNE_GRID") == "ff":  # + the current picks (volume first) fo
     GRID[0] = [dict(R=v["R"], S=v["S"], C=v["C"], M=v["M"], Q=v["Q"], F=0) for k, v in _cur.items()
                if not k.startswith("_")]
 if os.environ.get("TUNE_GRID") == "og":  # tensor-core paths, flux first, operators via L1 (G=1)
-    GRID = {4: [dict(R=8, S=s, C=c, M=m, Q=1, F=1, G=1) for s, c, m in itertools.product((1, 2), (4, 5, 6, 8), (1, 2))]}
+    GRID = {4: [dict(R=8, S=s, C=c, M=m, Q=1, F=1, G=1) for s, c, m in itertools.product((1, 2), (4, 5, 6, 8), (1, 2))]
+            + [dict(R=8, S=1, C=c, M=1, Q=1, F=f, G=0) for c, f in itertools.product((3, 4), (0, 1))]}
+if os.environ.get("TUNE_GRID", "").startswith("file:"):  # a JSON list of variant names (a confirmation run)
+    GRID = {0: [{x[0]: int(x[1:]) for x in v.split("_")} for v in json.load(open(os.environ["TUNE_GRID"][5:]))]}
 if os.environ.get("TUNE_GRID") == "tf":  # tensor-core variants (fp32 3xTF32, fp64 DMMA)
     GRID = {4: [dict(R=8, S=s, C=c, M=1, Q=q) for s, c, q in itertools.product((1, 2), (3, 4, 6), (0, 1))]}
 
