@@ -151,8 +151,12 @@ __host__ __device__ constexpr size_t slot_bytes(bool surf, bool mat, bool rk) {
   return QB + geo_bytes(mat) + (surf ? SPB : 0) + (RES_TMA && rk ? QB : 0);
 }
 constexpr size_t BARB = 64;  // mbarriers: one per slot
+// S = 3 is the split pipeline: two {q, geo} buffers (tile t+1's fields and geometry stream in
+// while t computes) and ONE {flux, residual} buffer, refilled in the tile's own flow (residual
+// by TMA at the start of the tile, next tile's neighbour gathers right after the LIFT).
 __host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat, bool rk) {
-  return BARB + OPB_SMEM + S * slot_bytes(surf, mat, rk);
+  return S == 3 ? BARB + OPB_SMEM + 2 * (QB + geo_bytes(mat)) + (surf ? SPB : 0) + (RES_TMA && rk ? QB : 0)
+                : BARB + OPB_SMEM + S * slot_bytes(surf, mat, rk);
 }
 // Slots per team: 2 = double-buffered (tile t+1 streams in while t computes), 1 = latency
 // hidden across resident teams instead.  Measured at C4 (N=5): fp32 is issue-bound and
@@ -448,11 +452,12 @@ __device__ __forceinline__ void tmma3(float (&c)[4], const uint32_t (&ah)[4], co
 // (DG_MMA=1: P = 2 warps, one per m-tile), 1 = Hx, Hy (from u, v) and 2 = Ez (from w)
 // (DG_MMA=2: P = 4 warps, m-tile x field set: half the registers per warp, twice the warps).
 // C-fragment register r of n-tile nt is element ee[r >> 1], row 8nt + 2(lane%4) + (r & 1).
-template <int MODE, bool MAT, int FS, typename TT>
+template <int MODE, bool MAT, int FS, typename TT, typename HOOK>
 __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
                                         TT* __restrict__ sp, const TT* __restrict__ sr,
                                         const unsigned char* __restrict__ ops, const int32_t (&vmc)[KPT],
-                                        int tile, int g, int mt, int lane, TT alpha, bool read_res) {
+                                        int tile, int g, int mt, int lane, TT alpha, bool read_res,
+                                        const HOOK& after_lift) {
   using MT = ModeTraits<MODE>;
   constexpr int NFLD = FS == 0 ? 3 : (FS == 1 ? 2 : 1);  // output fields F0 .. F0 + NFLD - 1
   constexpr int F0 = FS == 2 ? 2 : 0;
@@ -592,6 +597,7 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
       }
     }
   }
+  after_lift();  // split pipeline (S = 3): the flux buffer is free, the residual must be in
   if constexpr (MAT) {
     if (MODE != dg::MODE_VOLUME || p.scale_volume) {
 #pragma unroll
@@ -675,11 +681,11 @@ __device__ __forceinline__ void lift_rows(const T* __restrict__ sp, const LVT* _
 // and the element pairs e = 8nt + 2(lane%4) + {0,1}; stores are 16 B pairs (e, e+1 stay
 // adjacent under the column swizzle).  FS = field set (volume_mma): DG_MMA=2 gives each
 // row group two warps, one for Hx, Hy and one for Ez.
-template <int MODE, bool MAT, int FS, typename TT>
+template <int MODE, bool MAT, int FS, typename TT, typename HOOK>
 __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
                                          TT* __restrict__ sp, const unsigned char* __restrict__ ops,
                                          const int32_t (&vmc)[KPT], int tile, int g, int rg, int lane, TT alpha,
-                                         bool read_res) {
+                                         bool read_res, const HOOK& after_lift) {
   using MT = ModeTraits<MODE>;
   using V2 = typename std::conditional<sizeof(TT) == 8, double2, float2>::type;
   constexpr bool ACT[3] = {FS != 2, FS != 2, FS != 1};  // output fields of this warp
@@ -741,6 +747,7 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
     }
     lift_mma<FS>(sp, reinterpret_cast<const TT*>(ops + DVB), rg, lane, rhx, rhy, rez);
   }
+  after_lift();
   if constexpr (MAT) {
     if (MODE != dg::MODE_VOLUME || p.scale_volume) {
 #pragma unroll
@@ -819,10 +826,15 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   const LV_t* LV = reinterpret_cast<const LV_t*>(smem_raw + BARB + DVB);
   unsigned char* slots = smem_raw + BARB + OPB_SMEM;
   const unsigned char* opsrc = OPS_GLOBAL ? static_cast<const unsigned char*>(p.ops) : smem_raw + BARB;
-  auto sq_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT); };
-  auto sg_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB); };
-  auto sp_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB + GB); };
-  auto sr_of = [&](int s) { return reinterpret_cast<T*>(slots + s * SLOT + QB + GB + (MT::surf ? SPB : 0)); };
+  constexpr bool S3 = S == 3;      // split pipeline: slots A0, A1 = {q, geo}; one B = {flux, residual}
+  constexpr size_t AB = QB + GB;
+  auto sq_of = [&](int s) { return reinterpret_cast<T*>(slots + (S3 ? s * AB : s * SLOT)); };
+  auto sg_of = [&](int s) { return reinterpret_cast<T*>(slots + (S3 ? s * AB : s * SLOT) + QB); };
+  auto sp_of = [&](int s) { return reinterpret_cast<T*>(slots + (S3 ? 2 * AB : s * SLOT + QB + GB)); };
+  auto sr_of = [&](int s) {
+    return reinterpret_cast<T*>(slots + (S3 ? 2 * AB : s * SLOT + QB + GB) + (MT::surf ? SPB : 0));
+  };
+  auto slot_of_it = [&](int it) { return S3 ? (it & 1) : it % S; };
   const bool read_res = MT::rk && p.a != 0.0;
   const int g = tid >> 5, lane = tid & 31;
 
@@ -841,13 +853,14 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       }
     }
   };
-  // fields + geometry of tile `it`: four TMA bulk copies issued by one thread
+  // fields + geometry of tile `it`: four TMA bulk copies issued by one thread (with S != 3 the
+  // residual too, on the same barrier)
   auto issue_tma = [&](int it) {
     if (tid == 0) {
       const int tile = tile_of(it);
-      const int s = it % S;
+      const int s = slot_of_it(it);
       uint64_t* bar = bars + s;
-      constexpr bool rt = RES_TMA && MT::rk;
+      constexpr bool rt = RES_TMA && MT::rk && !S3;
       mbar_expect_tx(bar, (unsigned)(QB + GB + (rt && read_res ? QB : 0)));
       T* sq = sq_of(s);
 #pragma unroll
@@ -860,6 +873,17 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
         for (int c = 0; c < 3; ++c)
           tma_load_1d(sr_of(s) + c * NP * TL, res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bar);
       }
+    }
+  };
+  // S = 3: the residual of tile `it` into the B buffer, on barrier 2
+  auto issue_res = [&](int it) {
+    if (RES_TMA && MT::rk && S3 && tid == 0 && read_res) {
+      const int tile = tile_of(it);
+      const T* res = static_cast<const T*>(p.res);
+      mbar_expect_tx(bars + 2, (unsigned)QB);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        tma_load_1d(sr_of(0) + c * NP * TL, res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bars + 2);
     }
   };
   // one slot: pull the next tile's TMA sources into L2 while this tile computes, so the TMA
@@ -880,7 +904,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   // cross-tile neighbour traces of tile `it` (same-tile ones are read from shared memory)
   auto issue_gather = [&](int it, const int32_t (&v)[KPT]) {
     if constexpr (MT::surf) {
-      T* sp = sp_of(it % S) + lane;
+      T* sp = sp_of(slot_of_it(it)) + lane;
 #pragma unroll
       for (int k = 0; k < KPT; ++k) {
         const int m = point_of(g, k);
@@ -896,7 +920,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
 
   // prologue: barriers, operators (once per persistent CTA), zero flux pad columns, first tiles
   if (tid == 0) {
-    for (int b = 0; b < S; ++b) mbar_init(bars + b, 1);
+    for (int b = 0; b < S; ++b) mbar_init(bars + b, 1);  // S = 3: A0, A1, residual
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   {
@@ -905,7 +929,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     for (int i = tid; i < (int)(OPB_SMEM / 16); i += TEAM) cp_async16(dst + i, src + i);
     if constexpr (MT::surf && NFE > NF) {
       constexpr int PADN = (NFE - NF) * TL;
-      for (int i = tid; i < S * 3 * PADN; i += TEAM) {
+      for (int i = tid; i < (S3 ? 1 : S) * 3 * PADN; i += TEAM) {
         const int s = i / (3 * PADN), rem = i - s * 3 * PADN;
         const int c = rem / PADN, rem2 = rem - c * PADN;
         sp_of(s)[(c * NFE + NF) * TL + rem2] = T(0);
@@ -925,9 +949,9 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   const int n0 = g * R;
   const T alpha = static_cast<T>(p.alpha);
   for (int it = 0; it < n_it; ++it) {
-    const int s = it % S;
-    cp_async_wait_all();                            // gathers of tile it
-    mbar_wait(bars + s, (unsigned)((it / S) & 1));  // TMA: fields + geometry of tile it
+    const int s = slot_of_it(it);
+    cp_async_wait_all();                                                   // gathers of tile it
+    mbar_wait(bars + s, (unsigned)(S3 ? (it >> 1) & 1 : (it / S) & 1));  // TMA: fields + geometry of tile it
     __syncthreads();
     const int tile = tile_of(it);
     if (S == 2 && it + 1 < n_it) {
@@ -935,9 +959,23 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       issue_gather(it + 1, vc1);
       cp_async_commit();
     }
+    if (S3) {
+      if (it + 1 < n_it) issue_tma(it + 1);  // into the other {q, geo} buffer (its tile it-1 is done)
+      issue_res(it);                         // B's residual: read by this tile's epilogue only
+    }
     if (S == 1 && it + 1 < n_it) prefetch_l2(it + 1);  // its TMA is issued after this tile
-    if (S == 2 && it + 2 < n_it) prefetch_l2(it + 2);  // its TMA is issued at the next tile
+    if (S != 1 && it + 2 < n_it) prefetch_l2(it + 2);  // its TMA is issued at the next tile
     if (it + 2 < n_it) load_codes(it + 2, vc2);
+    // after the LIFT (S = 3): every warp is done with the flux buffer -> the next tile's
+    // neighbour gathers go into it; the epilogue then needs this tile's residual
+    auto after_lift = [&]() {
+      if constexpr (S3) {
+        __syncthreads();
+        if (it + 1 < n_it) issue_gather(it + 1, vc1);
+        cp_async_commit();
+        if (RES_TMA && MT::rk && read_res) mbar_wait(bars + 2, (unsigned)(it & 1));
+      }
+    };
 
     const T* sq = sq_of(s);
     const T* gg = sg_of(s) + lane;
@@ -945,20 +983,20 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     if constexpr (USE_MMA) {
       if constexpr (DMMA_SPLIT) {
         if (g < PR)
-          mma_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, opsrc, vc0, tile, g, g, lane, alpha, read_res);
+          mma_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, opsrc, vc0, tile, g, g, lane, alpha, read_res, after_lift);
         else
-          mma_tile<MODE, MAT, 2>(p, sq, sg_of(s), sp, opsrc, vc0, tile, g, g - PR, lane, alpha, read_res);
+          mma_tile<MODE, MAT, 2>(p, sq, sg_of(s), sp, opsrc, vc0, tile, g, g - PR, lane, alpha, read_res, after_lift);
       } else {
-        mma_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, opsrc, vc0, tile, g, g, lane, alpha, read_res);
+        mma_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, opsrc, vc0, tile, g, g, lane, alpha, read_res, after_lift);
       }
     } else if constexpr (USE_TF) {
       if constexpr (TF_SPLIT) {
         if (g < 2)
-          tf_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, g & 1, lane, alpha, read_res);
+          tf_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, g & 1, lane, alpha, read_res, after_lift);
         else
-          tf_tile<MODE, MAT, 2>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, g & 1, lane, alpha, read_res);
+          tf_tile<MODE, MAT, 2>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, g & 1, lane, alpha, read_res, after_lift);
       } else {
-        tf_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, g, lane, alpha, read_res);
+        tf_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, g, lane, alpha, read_res, after_lift);
       }
     } else {
     if constexpr (FLUX_FIRST && MT::surf) {
@@ -1002,6 +1040,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       }
       lift_rows(sp, LV, n0, lane, rhx, rhy, rez);
     }
+    after_lift();
     // material factors 1/mu, 1/eps (reading A12).  In split mode the volume kernel
     // writes the UNSCALED rhsV and the surface kernel scales the sum.
     if constexpr (MAT) {

@@ -29,7 +29,7 @@ def launches(path):
 
 
 def main():
-    out = os.path.join(ROOT, "profiles", "traffic.json")
+    out = os.environ.get("TRAFFIC_OUT", os.path.join(ROOT, "profiles", "traffic.json"))
     tab = json.load(open(out)) if os.path.exists(out) else {}
     tab["_doc"] = ("DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the fused "
                    "stage kernel, ncu --set full, mean over the 5 launches (LSERK4 stages) of one step "
