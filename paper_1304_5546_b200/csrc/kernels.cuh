@@ -180,6 +180,27 @@ __device__ __forceinline__ int point_of(int g, int k) {  // face point of slot k
   if constexpr (FACE_MAJOR) return (k / KPF) * NFP + g + (k % KPF) * P;
   else return g + k * P < NF ? g + k * P : NF;
 }
+// DG_FX (3xTF32 path, one warp per m-tile): the flux is computed straight into the LIFT
+// A fragments -- lane (grp, tig) of m-tile warp g owns the (element, face point) pairs
+// e = 16g + grp (+8), m = 8ks + tig (+4) -- so the flux never goes through shared memory
+// and no barrier separates the flux from the LIFT.  The lane also gathers its own
+// cross-tile neighbour traces (cp.async into the flux buffer, read back by the same lane).
+#ifndef DG_FX
+#define DG_FX 0
+#endif
+constexpr bool FX = F32 && DG_MMA == 1 && DG_FX;
+constexpr int KLT_ = (NF + 7) / 8;
+constexpr int KCODE = FX ? 4 * KLT_ : KPT;  // codes per thread
+struct PointElem { int m, e; };
+__device__ __forceinline__ PointElem pair_of(int g, int lane, int k) {  // m = NF: no point
+  if constexpr (FX) {
+    const int ks = k >> 2, r = k & 3;
+    const int m = 8 * ks + (lane & 3) + 4 * (r >> 1);
+    return {m < NF ? m : NF, 16 * g + (lane >> 2) + 8 * (r & 1)};
+  } else {
+    return {point_of(g, k), lane};
+  }
+}
 
 // Face node ids, increasing node index (closed form of the node ordering: row j
 // of the triangle starts at j(N+1) - j(j-1)/2).  Checked against the setup's
@@ -301,41 +322,49 @@ __device__ __forceinline__ void volume_rows(const T* __restrict__ sq, const DVT*
 // Neighbour index codes (vmapP, runtime.cu): >= 0 an offset into a field in
 // global memory (gathered into sp); < 0 a neighbour in the SAME tile, read
 // straight from the tile's shared-memory fields at offset -(1 + code).
+// The flux of face point m (face f) of tile element e: gg = the tile's geometry + e.
+template <bool MAT, typename TT>
+__device__ __forceinline__ void flux_one(const TT* __restrict__ sq, const TT* __restrict__ gg,
+                                         const TT* __restrict__ sp, int code, int m, int f, int e, TT alpha,
+                                         TT& fHx, TT& fHy, TT& fEz) {
+    const int i = m - f * NFP;
+    const int fm = f == 0 ? i : (f == 1 ? row_start(i) + N - i : row_start(i));
+    const TT nx = gg[(4 + 3 * f) * TL], ny = gg[(5 + 3 * f) * TL], hF = gg[(6 + 3 * f) * TL];
+    const TT bsc = gg[(13 + f) * TL];
+    const int pm = m * TL + colx(m, e);                               // this point in sp
+    const TT* pp = code < 0 ? sq + (-1 - code) : sp + pm;             // neighbour trace, field 0
+    const int fs = code < 0 ? NP * TL : NFE * TL;                     // field stride of that source
+    const int om = fm * TL + colx(fm, e);                             // own face node in sq
+    const TT dHx = sq[0 * NP * TL + om] - pp[0];
+    const TT dHy = sq[1 * NP * TL + om] - pp[fs];
+    const TT dEz = sq[2 * NP * TL + om] - bsc * pp[2 * fs];
+    if constexpr (!MAT) {
+      const TT ndotdH = nx * dHx + ny * dHy;
+      fHx = hF * (ny * dEz + alpha * (nx * ndotdH - dHx));
+      fHy = hF * (-nx * dEz + alpha * (ny * ndotdH - dHy));
+      fEz = hF * (ny * dHx - nx * dHy - alpha * dEz);
+    } else {
+      const TT wEH = gg[(18 + 4 * f) * TL], wHH = gg[(19 + 4 * f) * TL];
+      const TT wHE = gg[(20 + 4 * f) * TL], wEE = gg[(21 + 4 * f) * TL];
+      const TT dHt = nx * dHy - ny * dHx;
+      const TT gH = wEH * dEz + wHH * dHt;
+      fHx = hF * (ny * gH);
+      fHy = -hF * (nx * gH);
+      fEz = -hF * (wHE * dHt + wEE * dEz);
+    }
+}
+
 template <bool MAT>
 __device__ __forceinline__ void flux_points(const T* __restrict__ sq, const T* __restrict__ gg, T* __restrict__ sp,
-                                            const int32_t (&vmc)[KPT], int g, int lane, T alpha) {
+                                            const int32_t (&vmc)[KCODE], int g, int lane, T alpha) {
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
     const int m = point_of(g, k);
     if (m >= NF) break;
     const int f = FACE_MAJOR ? k / KPF : (m < NFP ? 0 : (m < 2 * NFP ? 1 : 2));  // compile-time if face-major
-    const int i = m - f * NFP;
-    const int fm = f == 0 ? i : (f == 1 ? row_start(i) + N - i : row_start(i));
-    const T nx = gg[(4 + 3 * f) * TL], ny = gg[(5 + 3 * f) * TL], hF = gg[(6 + 3 * f) * TL];
-    const T bsc = gg[(13 + f) * TL];
-    const int code = vmc[k];
-    const int pm = m * TL + colx(m, lane);                            // this point in sp
-    const T* pp = code < 0 ? sq + (-1 - code) : sp + pm;              // neighbour trace, field 0
-    const int fs = code < 0 ? NP * TL : NFE * TL;                     // field stride of that source
-    const int om = fm * TL + colx(fm, lane);                          // own face node in sq
-    const T dHx = sq[0 * NP * TL + om] - pp[0];
-    const T dHy = sq[1 * NP * TL + om] - pp[fs];
-    const T dEz = sq[2 * NP * TL + om] - bsc * pp[2 * fs];
     T fHx, fHy, fEz;
-    if constexpr (!MAT) {
-      const T ndotdH = nx * dHx + ny * dHy;
-      fHx = hF * (ny * dEz + alpha * (nx * ndotdH - dHx));
-      fHy = hF * (-nx * dEz + alpha * (ny * ndotdH - dHy));
-      fEz = hF * (ny * dHx - nx * dHy - alpha * dEz);
-    } else {
-      const T wEH = gg[(18 + 4 * f) * TL], wHH = gg[(19 + 4 * f) * TL];
-      const T wHE = gg[(20 + 4 * f) * TL], wEE = gg[(21 + 4 * f) * TL];
-      const T dHt = nx * dHy - ny * dHx;
-      const T gH = wEH * dEz + wHH * dHt;
-      fHx = hF * (ny * gH);
-      fHy = -hF * (nx * gH);
-      fEz = -hF * (wHE * dHt + wEE * dEz);
-    }
+    flux_one<MAT>(sq, gg, sp, vmc[k], m, f, lane, alpha, fHx, fHy, fEz);
+    const int pm = m * TL + colx(m, lane);
     sp[0 * NFE * TL + pm] = fHx;
     sp[1 * NFE * TL + pm] = fHy;
     sp[2 * NFE * TL + pm] = fEz;
@@ -455,7 +484,7 @@ __device__ __forceinline__ void tmma3(float (&c)[4], const uint32_t (&ah)[4], co
 template <int MODE, bool MAT, int FS, typename TT, typename HOOK>
 __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
                                         TT* __restrict__ sp, const TT* __restrict__ sr,
-                                        const unsigned char* __restrict__ ops, const int32_t (&vmc)[KPT],
+                                        const unsigned char* __restrict__ ops, const int32_t (&vmc)[KCODE],
                                         int tile, int g, int mt, int lane, TT alpha, bool read_res,
                                         const HOOK& after_lift) {
   using MT = ModeTraits<MODE>;
@@ -482,7 +511,7 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
   }
   auto row_ok = [&](int nt, int r) { return NT * 8 == NP || nt < NT - 1 || 8 * nt + 2 * tig + (r & 1) < NP; };
   const int64_t tbase = (int64_t)tile * NP * TL;
-  if constexpr (FLUX_FIRST && MT::surf) {
+  if constexpr (FLUX_FIRST && MT::surf && !FX) {
     flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
     __syncthreads();
   }
@@ -575,7 +604,7 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
     }
   }
   if constexpr (MT::surf) {
-    if constexpr (!FLUX_FIRST) {
+    if constexpr (!FLUX_FIRST && !FX) {
       flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
       __syncthreads();
     }
@@ -585,9 +614,20 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
       uint32_t fh[NFLD][4], fl[NFLD][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const TT* a = sp + abase[r >> 1][r & 1] + (8 * ks + 4 * (r >> 1)) * TL;
+        if constexpr (FX) {  // A register r: element ee[r & 1], face point 8ks + tig + 4(r >> 1)
+          const int m = 8 * ks + tig + 4 * (r >> 1);
+          TT fv[3] = {TT(0), TT(0), TT(0)};
+          if (m < NF) {
+            const int f = m < NFP ? 0 : (m < 2 * NFP ? 1 : 2);
+            flux_one<MAT>(sq, sg + ee[r & 1], sp, vmc[4 * ks + r], m, f, ee[r & 1], alpha, fv[0], fv[1], fv[2]);
+          }
 #pragma unroll
-        for (int f = 0; f < NFLD; ++f) split_tf32(a[(F0 + f) * NFE * TL], fh[f][r], fl[f][r]);
+          for (int f = 0; f < NFLD; ++f) split_tf32(fv[F0 + f], fh[f][r], fl[f][r]);
+        } else {
+          const TT* a = sp + abase[r >> 1][r & 1] + (8 * ks + 4 * (r >> 1)) * TL;
+#pragma unroll
+          for (int f = 0; f < NFLD; ++f) split_tf32(a[(F0 + f) * NFE * TL], fh[f][r], fl[f][r]);
+        }
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
@@ -684,7 +724,7 @@ __device__ __forceinline__ void lift_rows(const T* __restrict__ sp, const LVT* _
 template <int MODE, bool MAT, int FS, typename TT, typename HOOK>
 __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
                                          TT* __restrict__ sp, const unsigned char* __restrict__ ops,
-                                         const int32_t (&vmc)[KPT], int tile, int g, int rg, int lane, TT alpha,
+                                         const int32_t (&vmc)[KCODE], int tile, int g, int rg, int lane, TT alpha,
                                          bool read_res, const HOOK& after_lift) {
   using MT = ModeTraits<MODE>;
   using V2 = typename std::conditional<sizeof(TT) == 8, double2, float2>::type;
@@ -843,13 +883,13 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     return p.tiles ? p.tiles[sidx] : sidx;
   };
   // vmapP codes of this thread's face points (m = g + k P) of tile `it`
-  auto load_codes = [&](int it, int32_t (&v)[KPT]) {
+  auto load_codes = [&](int it, int32_t (&v)[KCODE]) {
     if constexpr (MT::surf) {
-      const int32_t* src = p.vmapP + (int64_t)tile_of(it) * NF * TL + lane;
+      const int32_t* src = p.vmapP + (int64_t)tile_of(it) * NF * TL;
 #pragma unroll
-      for (int k = 0; k < KPT; ++k) {
-        const int m = point_of(g, k);
-        v[k] = m < NF ? __ldg(src + m * TL) : -1;
+      for (int k = 0; k < KCODE; ++k) {
+        const PointElem pe = pair_of(g, lane, k);
+        v[k] = pe.m < NF ? __ldg(src + pe.m * TL + pe.e) : -1;
       }
     }
   };
@@ -902,15 +942,15 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     }
   };
   // cross-tile neighbour traces of tile `it` (same-tile ones are read from shared memory)
-  auto issue_gather = [&](int it, const int32_t (&v)[KPT]) {
+  auto issue_gather = [&](int it, const int32_t (&v)[KCODE]) {
     if constexpr (MT::surf) {
-      T* sp = sp_of(slot_of_it(it)) + lane;
+      T* sp = sp_of(slot_of_it(it));
 #pragma unroll
-      for (int k = 0; k < KPT; ++k) {
-        const int m = point_of(g, k);
-        if (m < NF && v[k] >= 0) {
+      for (int k = 0; k < KCODE; ++k) {
+        const PointElem pe = pair_of(g, lane, k);
+        if (pe.m < NF && v[k] >= 0) {
           const T* src = q + v[k];
-          T* dst = sp - lane + m * TL + colx(m, lane);
+          T* dst = sp + pe.m * TL + colx(pe.m, pe.e);
 #pragma unroll
           for (int c = 0; c < 3; ++c) cp_async_small<sizeof(T)>(dst + c * NFE * TL, src + c * p.fstride);
         }
@@ -939,7 +979,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  int32_t vc0[KPT], vc1[KPT], vc2[KPT];  // codes of tiles it, it+1, it+2
+  int32_t vc0[KCODE], vc1[KCODE], vc2[KCODE];  // codes of tiles it, it+1, it+2
   load_codes(0, vc0);
   if (n_it > 1) load_codes(1, vc1);
   issue_tma(0);
@@ -1088,7 +1128,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       cp_async_commit();
     }
 #pragma unroll
-    for (int k = 0; k < KPT; ++k) { vc0[k] = vc1[k]; vc1[k] = vc2[k]; }
+    for (int k = 0; k < KCODE; ++k) { vc0[k] = vc1[k]; vc1[k] = vc2[k]; }
   }
 }
 
