@@ -388,3 +388,25 @@ def test_c5w_full_size_sampled_one_step():
         scale = max(np.abs(a).max() for a in q1)  # reading A14' (state-relative), as the C4 test
         for F in range(3):
             assert np.abs(got[F][k] - q1[F][loc]).max() <= 1e-12 * scale, (k, F)
+
+
+def test_h_convergence_against_exact_mode_on_gpu():
+    """Config C3's property at test size: N=5 fp64 against the exact cavity mode (2, 2) after one
+    period, n = 8, 16, 32; the observed L2 order (library mass-matrix norm via dg_energy) is
+    ~N+1 = 6 (tools/convergence_c3.py runs the full K = 2k..512k study: 5.91-6.00)."""
+    N, mode = 5, (2, 2)
+    T = 2 * math.pi / (math.pi * math.hypot(*mode))
+    errs = []
+    for n in (8, 16, 32):
+        VX, VY, E = dginputs.rect_mesh(n)
+        steps = int(math.ceil(T / (dginputs.cfl_dt(VX, VY, E, N) * min(1.0, math.sqrt(8.0 / n)))))
+        c = dg.dg_setup(N, VX, VY, E, precision=8)
+        x, y = c.nodes()
+        c.set_fields(*dginputs.cavity_mode(x, y, 0.0, *mode))
+        c.run(T / steps, steps)
+        got = c.get_fields()
+        c.set_fields(*(a - b for a, b in zip(got, dginputs.cavity_mode(x, y, T, *mode))))
+        errs.append(math.sqrt(2.0 * c.energy()))
+        c.destroy()
+    orders = [math.log2(a / b) for a, b in zip(errs, errs[1:])]
+    assert min(orders) >= N + 0.5, (errs, orders)
