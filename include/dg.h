@@ -208,7 +208,9 @@ typedef struct {
   int32_t teams_cap;     /* cap on resident CTAs per SM (launch bounds) */
   int32_t flags;         /* bit 0: flux phase before the volume phase (knob F);
                             bit 1: tensor-core operator fragments read through L1 from global
-                            memory instead of a shared-memory copy per CTA (knob G) */
+                            memory instead of a shared-memory copy per CTA (knob G);
+                            bit 2: flux computed straight into the LIFT A fragments (knob X);
+                            bit 3: 3xTF32 products issued pass by pass (knob I) */
   int64_t smem_bytes;    /* dynamic shared memory per CTA of the fused stage kernel */
 } dg_kernel_config;
 dg_status dg_get_kernel_config(const dg_ctx* c, dg_kernel_config* out);

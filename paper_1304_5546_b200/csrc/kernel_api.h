@@ -60,7 +60,7 @@ struct KernelInfo {
   int contraction;   // 0 FMA, 1 fp64 DMMA, 2 fp32 3xTF32 (dg.h dg_kernel_config)
   int residual_tma;  // LSERK4 residual staged by TMA
   int teams_cap;     // DG_C
-  int flags;         // bit 0 DG_FF (flux first), bit 1 DG_OG (operators via L1)
+  int flags;         // bit 0 DG_FF (flux first), bit 1 DG_OG (operators via L1), bit 2 DG_FX, bit 3 DG_IL
 };
 
 struct KernelModule {

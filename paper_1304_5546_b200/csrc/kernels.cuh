@@ -189,6 +189,13 @@ __device__ __forceinline__ int point_of(int g, int k) {  // face point of slot k
 #define DG_FX 0
 #endif
 constexpr bool FX = F32 && DG_MMA == 1 && DG_FX;
+// DG_IL (3xTF32 path): issue the three split products pass by pass across all n-tiles and
+// accumulators (lo*hi for all, then hi*lo, then hi*hi) instead of accumulator by accumulator,
+// so consecutive MMAs into one accumulator are NT x fields instructions apart
+#ifndef DG_IL
+#define DG_IL 0
+#endif
+constexpr bool IL = DG_IL;
 constexpr int KLT_ = (NF + 7) / 8;
 constexpr int KCODE = FX ? 4 * KLT_ : KPT;  // codes per thread
 struct PointElem { int m, e; };
@@ -547,6 +554,33 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
           split_tf32(sxe[i] * hy - sye[i] * hx, w2h[r], w2l[r]);
         }
       }
+      if constexpr (IL) {
+        float4 bh[NT], bl[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          bh[nt] = ldop(BV + (ks * NT + nt) * 64);
+          bl[nt] = ldop(BV + (ks * NT + nt) * 64 + 32);
+        }
+        auto U = [](float x) { return __float_as_uint(x); };
+        // pass p: (A part, B part) = (lo, hi), (hi, lo), (hi, hi); small terms first
+#pragma unroll
+        for (int pass = 0; pass < 3; ++pass) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const float4 b = pass == 1 ? bl[nt] : bh[nt];
+            if constexpr (UV) {
+              tmma(acc[0][nt], pass == 0 ? ezl : ezh, U(b.x), U(b.y));
+              tmma(acc[1][nt], pass == 0 ? ezl : ezh, U(b.z), U(b.w));
+            }
+            if constexpr (WW) tmma(acc[NFLD - 1][nt], pass == 0 ? w1l : w1h, U(b.x), U(b.y));
+          }
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const float4 b = pass == 1 ? bl[nt] : bh[nt];
+            if constexpr (WW) tmma(acc[NFLD - 1][nt], pass == 0 ? w2l : w2h, U(b.z), U(b.w));
+          }
+        }
+      } else {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const float4 bh = ldop(BV + (ks * NT + nt) * 64);  // hi and lo: 32 lanes x 16 B contiguous each
@@ -559,6 +593,7 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
           tmma3(acc[NFLD - 1][nt], w1h, w1l, bh.x, bh.y, bl.x, bl.y);
           tmma3(acc[NFLD - 1][nt], w2h, w2l, bh.z, bh.w, bl.z, bl.w);
         }
+      }
       }
     }
     if constexpr (UV) {
@@ -629,11 +664,26 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
           for (int f = 0; f < NFLD; ++f) split_tf32(a[(F0 + f) * NFE * TL], fh[f][r], fl[f][r]);
         }
       }
+      if constexpr (IL) {
+        float4 b[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = ldop(BL + (ks * NT + nt) * 32);
+#pragma unroll
+        for (int pass = 0; pass < 3; ++pass)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int f = 0; f < NFLD; ++f) {
+              const float x = pass == 1 ? b[nt].z : b[nt].x, y = pass == 1 ? b[nt].w : b[nt].y;
+              tmma(acc[f][nt], pass == 0 ? fl[f] : fh[f], __float_as_uint(x), __float_as_uint(y));
+            }
+      } else {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const float4 b = ldop(BL + (ks * NT + nt) * 32);
 #pragma unroll
         for (int f = 0; f < NFLD; ++f) tmma3(acc[f][nt], fh[f], fl[f], b.x, b.y, b.z, b.w);
+      }
       }
     }
   }
@@ -1283,7 +1333,7 @@ dg::KernelInfo info() {
   k.contraction = USE_TF ? 2 : (USE_MMA ? 1 : 0);
   k.residual_tma = RES_TMA ? 1 : 0;
   k.teams_cap = DG_C;
-  k.flags = (FLUX_FIRST ? 1 : 0) | (OPS_GLOBAL ? 2 : 0);
+  k.flags = (FLUX_FIRST ? 1 : 0) | (OPS_GLOBAL ? 2 : 0) | (FX ? 4 : 0) | (USE_TF && IL ? 8 : 0);
   return k;
 }
 
