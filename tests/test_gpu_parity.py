@@ -105,7 +105,7 @@ def test_c1_100_steps(prec, fused):
 
 
 @pytest.mark.parametrize("prec", [8, 4])
-@pytest.mark.parametrize("N", [1, 3, 6, 9])
+@pytest.mark.parametrize("N", list(range(1, 10)))
 def test_order_sweep_run(N, prec):
     VX, VY, E = _jittered(9, seed=N)      # K = 162: 6 tiles, ragged tail
     o = Oracle(N, VX, VY, E)
