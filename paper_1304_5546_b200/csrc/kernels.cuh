@@ -118,7 +118,7 @@ constexpr size_t OPB = ((DVB + LVB + 15) / 16) * 16;
 #ifndef DG_OG
 #define DG_OG 0
 #endif
-constexpr bool OPS_GLOBAL = DG_OG && (DG_MMA != 0);
+constexpr bool OPS_GLOBAL = DG_OG;  // FMA path: the broadcast row loads go through L1 as well
 constexpr size_t OPB_SMEM = OPS_GLOBAL ? 0 : OPB;
 template <typename V>
 __device__ __forceinline__ V ldop(const V* p) {
@@ -290,7 +290,7 @@ __device__ __forceinline__ void volume_rows(const T* __restrict__ sq, const DVT*
       const T w11 = rx * hy1 - ry * hx1, w21 = sx * hy1 - sy * hx1;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const DVT d = DV[jc * RP + n0 + r];
+        const DVT d = ldop(DV + jc * RP + n0 + r);
         u[r] = fmaf(d.x, ez0, u[r]);
         v[r] = fmaf(d.y, ez0, v[r]);
         rez[r] = fmaf(d.x, w10, rez[r]);
@@ -308,7 +308,7 @@ __device__ __forceinline__ void volume_rows(const T* __restrict__ sq, const DVT*
       const T w1 = rx * hy - ry * hx, w2 = sx * hy - sy * hx;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const DVT d = DV[j * RP + n0 + r];
+        const DVT d = ldop(DV + j * RP + n0 + r);
         u[r] = fma(d.x, ez, u[r]);
         v[r] = fma(d.y, ez, v[r]);
         rez[r] = fma(d.x, w1, rez[r]);
@@ -741,7 +741,7 @@ __device__ __forceinline__ void lift_rows(const T* __restrict__ sp, const LVT* _
       const T c0 = sp[(2 * NFE + m0) * TL + lane], c1 = sp[(2 * NFE + m1) * TL + lane];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const LVT l = LV[mc * RPL + n0 + r];
+        const LVT l = ldop(LV + mc * RPL + n0 + r);
         rhx[r] = fmaf(l.x, a0, rhx[r]);
         rhy[r] = fmaf(l.x, b0, rhy[r]);
         rez[r] = fmaf(l.x, c0, rez[r]);
@@ -756,7 +756,7 @@ __device__ __forceinline__ void lift_rows(const T* __restrict__ sp, const LVT* _
       const T c0 = sp[(2 * NFE + m) * TL + lane];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const LVT l = LV[m * RPL + n0 + r];
+        const LVT l = ldop(LV + m * RPL + n0 + r);
         rhx[r] = fma(l, a0, rhx[r]);
         rhy[r] = fma(l, b0, rhy[r]);
         rez[r] = fma(l, c0, rez[r]);
@@ -912,8 +912,9 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   if (n_it == 0) return;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [0, S): slots, [S]: residual
-  const DV_t* DV = reinterpret_cast<const DV_t*>(smem_raw + BARB);
-  const LV_t* LV = reinterpret_cast<const LV_t*>(smem_raw + BARB + DVB);
+  const unsigned char* opbase = OPS_GLOBAL ? static_cast<const unsigned char*>(p.ops) : smem_raw + BARB;
+  const DV_t* DV = reinterpret_cast<const DV_t*>(opbase);
+  const LV_t* LV = reinterpret_cast<const LV_t*>(opbase + DVB);
   unsigned char* slots = smem_raw + BARB + OPB_SMEM;
   const unsigned char* opsrc = OPS_GLOBAL ? static_cast<const unsigned char*>(p.ops) : smem_raw + BARB;
   constexpr bool S3 = S == 3;      // split pipeline: slots A0, A1 = {q, geo}; one B = {flux, residual}

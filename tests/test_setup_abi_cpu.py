@@ -47,7 +47,7 @@ def test_kernel_config_matches_tune_table(prec):
         assert k["slots"] == t["S"] and k["teams_cap"] == t["C"]
         assert k["residual_tma"] == bool(t["M"] and prec == 4 and t.get("Q", 1))
         assert k["flux_first"] == bool(t.get("F", 0))
-        assert k["ops_global"] == bool(t["M"] and t.get("G", 0))
+        assert k["ops_global"] == bool(t.get("G", 0))
         assert k["flux_in_fragments"] == bool(t["M"] == 1 and prec == 4 and t.get("X", 0))
         assert k["pass_interleave"] == bool(t["M"] and prec == 4 and t.get("I", 0))
         assert 0 < k["smem_bytes"] <= 227 * 1024 and k["threads"] % 32 == 0
