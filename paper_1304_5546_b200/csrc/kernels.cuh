@@ -196,6 +196,17 @@ constexpr bool FX = F32 && DG_MMA == 1 && DG_FX;
 #define DG_IL 0
 #endif
 constexpr bool IL = DG_IL;
+// DG_WB: the stage's q_out and residual stores with the default (write-back) cache policy instead
+// of streaming (st.global.cs, evict-first), so the lines the stage writes last can stay in L2
+// for the next stage, which walks the tiles in the opposite order (StageArgs::reverse)
+#ifndef DG_WB
+#define DG_WB 0
+#endif
+template <typename V>
+__device__ __forceinline__ void st_out(V* p, const V& v) {
+  if constexpr (DG_WB) *p = v;
+  else __stcs(p, v);
+}
 constexpr int KLT_ = (NF + 7) / 8;
 constexpr int KCODE = FX ? 4 * KLT_ : KPT;  // codes per thread
 struct PointElem { int m, e; };
@@ -717,8 +728,8 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
           const int c = F0 + f;
           TT rs = dt * acc[f][nt][r];
           if (read_res) rs = fma(a, RES_TMA ? sr[c * NP * TL + o] : rr[f][nt][r], rs);
-          if (p.write_res) __stcs(res + c * p.vstride + o, rs);
-          __stcs(qo + c * p.fstride + o, fma(b, rs, sq[c * NP * TL + o]));
+          if (p.write_res) st_out(res + c * p.vstride + o, rs);
+          st_out(qo + c * p.fstride + o, fma(b, rs, sq[c * NP * TL + o]));
         }
       } else {
         TT* __restrict__ out = static_cast<TT*>(p.out) + tbase;
@@ -872,12 +883,12 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
           rs.x = fma(a, rr[c][nt].x, rs.x);
           rs.y = fma(a, rr[c][nt].y, rs.y);
         }
-        if (p.write_res) __stcs(reinterpret_cast<V2*>(res + c * p.vstride + off), rs);
+        if (p.write_res) st_out(reinterpret_cast<V2*>(res + c * p.vstride + off), rs);
         const V2 qi = *reinterpret_cast<const V2*>(sq + (c * NP + n) * TL + col);
         V2 qn;
         qn.x = fma(b, rs.x, qi.x);
         qn.y = fma(b, rs.y, qi.y);
-        __stcs(reinterpret_cast<V2*>(qo + c * p.fstride + off), qn);
+        st_out(reinterpret_cast<V2*>(qo + c * p.fstride + off), qn);
       }
     } else {
       TT* __restrict__ out = static_cast<TT*>(p.out);
@@ -931,7 +942,8 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
 
   auto tile_of = [&](int it) {
     const int sidx = first + it * stride;
-    return p.tiles ? p.tiles[sidx] : sidx;
+    const int j = p.reverse ? p.ntiles - 1 - sidx : sidx;
+    return p.tiles ? p.tiles[j] : j;
   };
   // vmapP codes of this thread's face points (m = g + k P) of tile `it`
   auto load_codes = [&](int it, int32_t (&v)[KCODE]) {
@@ -1155,8 +1167,8 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
         for (int c = 0; c < 3; ++c) {
           T rs = dt * rhs[c];
           if (read_res) rs = fma(a, rr[c][r], rs);
-          if (p.write_res) __stcs(res + c * p.vstride + off, rs);
-          __stcs(qo + c * p.fstride + off, fma(b, rs, sq[(c * NP + n) * TL + lane]));
+          if (p.write_res) st_out(res + c * p.vstride + off, rs);
+          st_out(qo + c * p.fstride + off, fma(b, rs, sq[(c * NP + n) * TL + lane]));
         }
       }
     } else {

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -277,6 +278,16 @@ dg_status launch_stage(dg_ctx* c, int mode, const dg::StageArgs& a, cudaStream_t
   return DG_OK;
 }
 
+// Odd LSERK4 stages walk the tiles last to first (StageArgs::reverse); DG_REVERSE=0 disables it
+// (measurement A/B).  The order of tiles does not change any result.
+bool reverse_order() {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_REVERSE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 dg::StageArgs base_args(dg_ctx* c) {
   dg::StageArgs a{};
   a.q_in = c->q[c->cur];
@@ -345,6 +356,7 @@ dg_status run_stage(dg_ctx* c, int i, double dt) {
   a.b = kRKb[i];
   a.dt = dt;
   a.write_res = i == 4 ? 0 : 1;  // the residual is dead after the last stage (a_0 = 0)
+  a.reverse = (i & 1) && reverse_order();
   const bool multi = c->nranks > 1 && c->transport == 0;
   dg_status st;
   if (multi) {
@@ -860,6 +872,7 @@ dg_status dg_run_group(dg_ctx* const* ctxs, int32_t n, double dt, int64_t nsteps
         a.b = kRKb[i];
         a.dt = dt;
         a.write_res = i == 4 ? 0 : 1;
+        a.reverse = (i & 1) && reverse_order();
         if (c->fused) {
           if ((st = launch_stage(c, dg::MODE_FUSED_RK, a, s, 0)) != DG_OK) return st;
         } else {
