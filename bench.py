@@ -40,6 +40,8 @@ import numpy as np  # noqa: E402
 import dginputs  # noqa: E402
 
 METRIC = "DG DOF-updates/s (fp32/fp64) and % of kernel roofline at 1/2/4/8 B200"
+L2_BYTES = 126 * 1024 * 1024
+FLUSH_BYTES = 512 * 1024 * 1024
 UNIT = "DOF-updates/s"
 
 
@@ -102,30 +104,74 @@ def flops_per_element_stage(N, kind="fused"):
     return vol + lift + flux + rk
 
 
+def physical_gpu(local_rank):
+    """The nvidia-smi / NVML id of this rank's GPU: CUDA_VISIBLE_DEVICES maps the visible ordinal
+    local_rank to a physical index or a GPU UUID (nvidia-smi -i accepts both)."""
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        if local_rank < len(ids):
+            return ids[local_rank]
+    return str(local_rank)
+
+
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 100 ms during the timed region."""
+    """SM clocks and clock-event (throttle) reasons of one GPU, sampled every 10 ms by NVML in a
+    thread (nvidia-smi every ~100 ms as a fallback); summary() keeps the samples taken inside the
+    timed window [t0, t1] (time.perf_counter)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    NAMES = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+             ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
-        self.index = index
-        self.samples = []
+    def __init__(self, gpu_id):
+        self.gpu_id = gpu_id
+        self.samples = []  # (t, sm_mhz, max_mhz, [reasons])
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self.source = None
 
-    def _run(self):
+    def _nvml(self):
+        import pynvml
+
+        pynvml.nvmlInit()
+        gid = self.gpu_id
+        if gid.startswith("GPU-") or gid.startswith("MIG-"):
+            h = pynvml.nvmlDeviceGetHandleByUUID(gid)
+        else:
+            h = pynvml.nvmlDeviceGetHandleByIndex(int(gid))
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        self.source = "nvml"
+        while not self._stop.is_set():
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append((time.perf_counter(), float(sm), float(mx),
+                                 [n for n, b in self.NAMES if bits & b]))
+            self._stop.wait(0.01)
+
+    def _smi(self):
+        self.source = "nvidia-smi"
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                out = subprocess.run(["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                v = [x.strip() for x in out.split(",")]
+                if len(v) >= 6:
+                    names = [n for n, _ in self.NAMES[:4]]
+                    self.samples.append((time.perf_counter(), float(v[0]), float(v[1]),
+                                         [n for n, x in zip(names, v[2:6]) if x == "Active"]))
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.05)
+
+    def _run(self):
+        try:
+            self._nvml()
+        except Exception:
+            if not self._stop.is_set():
+                self._smi()
 
     def __enter__(self):
         self._t.start()
@@ -135,15 +181,14 @@ class ClockSampler:
         self._stop.set()
         self._t.join(timeout=10)
 
-    def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for s in self.samples for n, v in zip(names, s[3:7]) if v.strip() == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+    def summary(self, t0=None, t1=None):
+        inside = [x for x in self.samples if (t0 is None or x[0] >= t0) and (t1 is None or x[0] <= t1)]
+        use = inside or self.samples
+        if not use:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "gpu": self.gpu_id}
+        return {"sm_mhz": statistics.median(x[1] for x in use), "sm_max_mhz": max(x[2] for x in use),
+                "reasons": sorted({r for x in use for r in x[3]}), "samples": len(use),
+                "samples_in_timed_region": len(inside), "source": self.source, "gpu": self.gpu_id}
 
 
 CONFIGS = {  # BASELINE.json configs shaped for one bench line (rank-level workloads)
@@ -178,53 +223,114 @@ def workload(args):
 
 
 def oracle_sample(N, n_sample, steps, material=False):
-    """Time the fp64 NumPy oracle (as it stands) on an n_sample x n_sample mesh."""
+    """Time the fp64 NumPy oracle (as it stands) on an n_sample x n_sample mesh, one thread
+    (BLAS pools limited to 1; the oracle's einsum contractions are single-threaded C loops)."""
+    from threadpoolctl import threadpool_limits
+
     from oracle.solver import Oracle
 
+    with threadpool_limits(limits=1):
+        VX, VY, E = dginputs.rect_mesh(n_sample)
+        eps = mu = None
+        if material:
+            eps, mu = dginputs.two_layer_material(VX, VY, E)
+        o = Oracle(N, VX, VY, E, eps=eps, mu=mu)
+        q = initial_fields(o.geo.x, o.geo.y, eps)
+        dt = dginputs.cfl_dt(VX, VY, E, N, eps=eps, mu=mu)
+        t0 = time.perf_counter()
+        o.run(q, dt, steps)
+        sec = time.perf_counter() - t0
+    dof = o.Np * o.K * 3 * 5 * steps
+    return dof / sec, sec, o.K
+
+
+def _oracle_worker(a):
+    return oracle_sample(*a)
+
+
+def oracle_all_cores(N, n_sample, steps, material=False, cores=None):
+    """The same bounded sample on every host core at once: `cores` independent oracle processes
+    (one per core, each single-threaded), throughput = their summed DOF-updates / wall time.
+    Returns (value, wall seconds, K, cores)."""
+    import multiprocessing as mp
+
+    cores = cores or os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        pool.map(_oracle_worker, [(1, 2, 1, False)] * cores)  # start-up + imports outside the clock
+        t0 = time.perf_counter()
+        res = pool.map(_oracle_worker, [(N, n_sample, steps, material)] * cores)
+        wall = time.perf_counter() - t0
+    Np = (N + 1) * (N + 2) // 2
+    dof = sum(Np * r[2] * 3 * 5 * steps for r in res)
+    return dof / wall, wall, res[0][2], cores
+
+
+def cpu_baseline(N, n_sample, steps, material=False):
+    """cpu_baseline of the bench line: the oracle on all host cores (headline) and on one."""
+    v1, sec1, Ks = oracle_sample(N, n_sample, steps, material)
+    va, wall, _, cores = oracle_all_cores(N, n_sample, steps, material)
+    return {"value": va, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"fp64 NumPy oracle, N={N}, K={Ks} ({n_sample}x{n_sample} A16 mesh)"
+                      f"{', two-layer material' if material else ''}, {steps} LSERK4 steps: "
+                      f"{cores} independent single-threaded processes at once ({wall:.1f} s wall)",
+            "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "seconds": sec1}}
+
+
+_REF = {}
+
+
+def _ref_init(N, n_sample, material):
+    """Reference-arm worker: build the oracle on the sample mesh once per process."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle.solver import Oracle
+
+    _REF["limits"] = threadpool_limits(limits=1)
     VX, VY, E = dginputs.rect_mesh(n_sample)
     eps = mu = None
     if material:
         eps, mu = dginputs.two_layer_material(VX, VY, E)
     o = Oracle(N, VX, VY, E, eps=eps, mu=mu)
-    q = initial_fields(o.geo.x, o.geo.y, eps)
-    dt = dginputs.cfl_dt(VX, VY, E, N, eps=eps, mu=mu)
-    t0 = time.perf_counter()
-    o.run(q, dt, steps)
-    sec = time.perf_counter() - t0
-    dof = o.Np * o.K * 3 * 5 * steps
-    return dof / sec, sec, o.K
+    _REF.update(o=o, q=initial_fields(o.geo.x, o.geo.y, eps), dt=dginputs.cfl_dt(VX, VY, E, N, eps=eps, mu=mu))
+
+
+def _ref_step(_):
+    o = _REF["o"]
+    _REF["q"] = o.run(_REF["q"], _REF["dt"], 1)
+    return o.Np * o.K * 3 * 5
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the fp64 NumPy oracle as it stands on every host core -- one
+    single-threaded process per core, each advancing its own copy of the bounded sample (an
+    n_sample x n_sample A16 mesh); one bench step = one LSERK4 step of every copy."""
     if rank != 0:
         return
+    import multiprocessing as mp
+
     N = args.order
     _, _, _, K, Np, _, name, _, _ = workload(args)
     n_sample = args.ref_n
-    from oracle.solver import Oracle
-
-    VX, VY, E = dginputs.rect_mesh(n_sample)
-    eps = mu = None
-    if args.material:
-        eps, mu = dginputs.two_layer_material(VX, VY, E)
-    o = Oracle(N, VX, VY, E, eps=eps, mu=mu)
-    q = initial_fields(o.geo.x, o.geo.y, eps)
-    dt = dginputs.cfl_dt(VX, VY, E, N, eps=eps, mu=mu)
-    for _ in range(args.warmup):
-        q = o.run(q, dt, 1)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        q = o.run(q, dt, 1)
-    sec = time.perf_counter() - t0
-    value = o.Np * o.K * 3 * 5 * args.steps / sec
-    sample = (f"fp64 NumPy oracle, N={N}, {n_sample}x{n_sample} A16 mesh (K={o.K}) per step"
-              f"{', two-layer material' if args.material else ''}, "
-              f"{args.steps} steps after {args.warmup} warm-up")
+    cores = os.cpu_count() or 1
+    with mp.get_context("spawn").Pool(cores, initializer=_ref_init, initargs=(N, n_sample, args.material)) as pool:
+        for _ in range(args.warmup):
+            pool.map(_ref_step, range(cores), chunksize=1)
+        t0 = time.perf_counter()
+        dof = 0
+        for _ in range(args.steps):
+            dof += sum(pool.map(_ref_step, range(cores), chunksize=1))
+        sec = time.perf_counter() - t0
+    value = dof / sec
+    Ks = 2 * n_sample * n_sample
+    sample = (f"fp64 NumPy oracle, N={N}, {n_sample}x{n_sample} A16 mesh (K={Ks}) per process"
+              f"{', two-layer material' if args.material else ''}, {cores} single-threaded processes (one per "
+              f"host core), {args.steps} steps after {args.warmup} warm-up")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": name, "reference_sample_K": o.K},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "data": "synthetic", "config": {"workload": name, "reference_sample_K": Ks, "processes": cores},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -259,6 +365,15 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # per-GPU working set (q ping-pong + residual + geometry + neighbour codes): when it is not
+    # well above the 126 MB L2, the timed steps are separated by an L2 flush (a 512 MB write
+    # outside the event brackets) so every step starts from HBM
+    s = args.prec
+    K_local = ctx.K_local
+    ngeo = 32 if args.material else 16
+    ws_bytes = 9 * K_local * Np * s + ngeo * K_local * s + 3 * (args.order + 1) * 4 * K_local
+    flush = ws_bytes < 2 * L2_BYTES
+    fbuf = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device="cuda") if flush else None
     # warm-up
     ctx.run(dt, args.warmup)
     ctx.sync()
@@ -266,20 +381,33 @@ def run_ours(args, rank, world, local_rank):
     # library's stream; the statistics reset first so gpu_launches counts this region only
     ctx.profile(True)
     ctx.profile(False)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
-                      else local_rank) as clk:
-        time.sleep(0.3)
+    with ClockSampler(physical_gpu(local_rank)) as clk:
+        time.sleep(0.05)
         barrier()
         t_wall = time.perf_counter()
-        e0.record(stream)
-        ctx.run(dt, args.steps)
-        e1.record(stream)
-        e1.synchronize()
-        t_wall = time.perf_counter() - t_wall
+        if not flush:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.run(dt, args.steps)
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+        else:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            with torch.cuda.stream(stream):
+                for a, b in evs:
+                    fbuf.fill_(1.0)  # L2 flush, outside the bracket
+                    a.record(stream)
+                    ctx.run(dt, 1)
+                    b.record(stream)
+            evs[-1][1].synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in evs)
+        t_wall_end = time.perf_counter()
+        t_wall = t_wall_end - t_wall
         barrier()
-    ms = e0.elapsed_time(e1)
+    clocks = clk.summary(t_wall_end - t_wall, t_wall_end)
     launches = sum(v["launches"] for v in ctx.kernel_stats().values())
     kcfg = ctx.kernel_config()
     ctx.sync()
@@ -287,7 +415,13 @@ def run_ours(args, rank, world, local_rank):
     # event-record nodes around every launch (dg_profile), read back between steps
     prof_steps = min(args.steps, 20)
     ctx.profile(True)
-    ctx.run(dt, prof_steps)
+    if flush:
+        with torch.cuda.stream(stream):
+            for _ in range(prof_steps):
+                fbuf.fill_(1.0)
+                ctx.run(dt, 1)
+    else:
+        ctx.run(dt, prof_steps)
     stats = ctx.kernel_stats()
     ctx.profile(False)
     ctx.sync()
@@ -296,9 +430,7 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = Np * K * 3 * 5 * args.steps / (ms * 1e-3)
-    s = args.prec
     hbm, peak_src = peaks()
-    K_local = ctx.K_local
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             traffic_tab = json.load(fh)
@@ -360,24 +492,86 @@ def run_ours(args, rank, world, local_rank):
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, sec, Ks = oracle_sample(args.order, args.ref_n, args.ref_steps, args.material)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"fp64 NumPy oracle (single-threaded), N={args.order}, K={Ks} "
-                         f"({args.ref_n}x{args.ref_n} mesh), {args.ref_steps} LSERK4 steps, {sec:.1f} s"}
-    ws_mb = (2 * 3 * (K // world) * Np * s + 3 * (K // world) * Np * s) / 1e6
+        cpu = cpu_baseline(args.order, args.ref_n, args.ref_steps, args.material)
+    ws_mb = ws_bytes / 1e6
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.config == "c5w" else "strong", "vs_baseline": None,
             "dtype": "f32" if s == 4 else "f64", "data": "synthetic",
             "config": {"workload": name, "N": args.order, "K": K, "Np": Np, "dt": dt,
                        "variant": "split" if args.split else "fused", "parallelism": f"element-partition x{world}",
-                       "l2": f"no flush: per-GPU working set {ws_mb:.0f} MB > 126 MB L2",
+                       "l2": (f"L2 flushed between timed steps (512 MB write outside the event brackets): "
+                              f"per-GPU working set {ws_mb:.0f} MB is not > 2x the 126 MB L2") if flush else
+                             f"no flush: per-GPU working set {ws_mb:.0f} MB > 2x the 126 MB L2",
                        "contraction": {"fma": "CUDA-core FMA", "dmma_fp64": "fp64 tensor cores (DMMA)",
                                        "3xtf32": "fp32 via 3xTF32 tensor-core split (hi*hi+lo*hi+hi*lo, "
                                                  "fp32 accumulate)"}[kcfg["contraction"]],
                        "kernel_config": kcfg},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "wall_s_timed": t_wall}
+            "clocks": clocks, "wall_s_timed": t_wall}
+    print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(n):
+    """bench.py --gpus N without a launcher: re-run this command under torchrun, one rank per GPU
+    (the driver's own launch line: --nnodes=1 --master-addr 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def run_partitions_dry(args):
+    """P in-process partitions of the workload on one GPU, advanced by dg_run_group: the multi-GPU
+    data path (element partition, halo pack, interior-then-boundary tile-list launches) with the
+    NCCL transport replaced by device copies.  Not a scaling number: all P partitions share one GPU."""
+    import torch
+
+    from paper_1304_5546_b200 import dg
+
+    P = args.partitions
+    torch.cuda.set_device(0)
+    VX, VY, E, K, Np, dt, name, eps, mu = workload(args)
+    cs = [dg.dg_setup(args.order, VX, VY, E, eps=eps, mu=mu, precision=args.prec, device=0, rank=r, nranks=P,
+                      fused=not args.split, transport=1) for r in range(P)]
+    for c in cs:
+        x, y = c.nodes()
+        eps_l = None if eps is None else eps[c.local_elements()]
+        c.set_fields(*initial_fields(x, y, eps_l))
+    stream = torch.cuda.ExternalStream(cs[0].stream())
+    dg.dg_run_group(cs, dt, args.warmup)
+    torch.cuda.synchronize()
+    for c in cs:
+        c.profile(True)
+        c.profile(False)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(physical_gpu(0)) as clk:
+        t0 = time.perf_counter()
+        e0.record(stream)
+        dg.dg_run_group(cs, dt, args.steps)
+        e1.record(stream)
+        e1.synchronize()
+        t1 = time.perf_counter()
+    ms = e0.elapsed_time(e1)
+    launches = sum(v["launches"] for c in cs for v in c.kernel_stats().values())
+    halo = sum(c.n_halo_points for c in cs)
+    for c in cs:
+        c.destroy()
+    line = {"metric": METRIC, "value": Np * K * 3 * 5 * args.steps / (ms * 1e-3), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "none (dry run)", "vs_baseline": None, "dtype": "f32" if args.prec == 4 else "f64",
+            "data": "synthetic",
+            "config": {"workload": name, "N": args.order, "K": K, "variant": "split" if args.split else "fused",
+                       "parallelism": f"{P} in-process partitions on 1 GPU (transport 1: halo pack, device-copy "
+                                      f"exchange, interior then boundary tile-list launches)",
+                       "halo_points": halo},
+            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+            "clocks": clk.summary(t0, t1)}
     print(json.dumps(line), flush=True)
 
 
@@ -397,11 +591,16 @@ def main():
     ap.add_argument("--ref-n", type=int, default=48, help="oracle sample mesh cells per side")
     ap.add_argument("--ref-steps", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partitions", type=int, default=0,
+                    help="dry run of the multi-GPU data path on ONE GPU: P in-process partitions "
+                         "(transport 1, dg_run_group)")
     args = ap.parse_args()
     preset = CONFIGS.get(args.config, CONFIGS["c4"])
     for key, val in preset.items():
         if getattr(args, key) is None:
             setattr(args, key, val)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.partitions == 0:
+        spawn_ranks(args.gpus)  # does not return
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.config == "c5w" and args.n == CONFIGS["c5w"]["n"]:  # weak scaling: ~524k elements per GPU
         args.n = {1: 512, 2: 724, 4: 1024, 8: 1448}.get(world_env, int(round(512 * world_env ** 0.5)))
@@ -414,6 +613,9 @@ def main():
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.partitions > 0:
+        run_partitions_dry(args)
         return
     if world > 1:
         import torch

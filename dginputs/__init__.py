@@ -21,6 +21,10 @@ import math
 import numpy as np
 
 SEED = 20261017
+# Config C4 parity start time: the (1,1) cavity mode at phase w t0 = pi/4 (w = pi sqrt 2), where
+# |Ez| = cos(pi/4) and |H| = (pi/w) sin(pi/4) = 1/2 -- every field is O(1), so the per-field A14
+# quotient is well conditioned (A14)
+C4_T0 = 0.25 / math.sqrt(2.0)
 
 
 # ----------------------------------------------------------------------------
@@ -49,6 +53,17 @@ def rect_mesh(nx: int, ny: int | None = None, x0=0.0, x1=1.0, y0=0.0, y1=1.0):
     EToV[0::2] = np.stack([v00, v10, v11], axis=1)
     EToV[1::2] = np.stack([v00, v11, v01], axis=1)
     return VX, VY, EToV
+
+
+def jittered_mesh(n: int, amp=0.25, seed=7):
+    """The A16 n x n mesh with every interior vertex moved by a seeded uniform offset of up to
+    amp/n in x and y (general affine elements: no two share a Jacobian)."""
+    VX, VY, E = rect_mesh(n)
+    rng = np.random.default_rng(seed)
+    inner = (VX > 0) & (VX < 1) & (VY > 0) & (VY < 1)
+    VX = VX + amp / n * rng.uniform(-1, 1, VX.shape) * inner
+    VY = VY + amp / n * rng.uniform(-1, 1, VY.shape) * inner
+    return VX, VY, E
 
 
 def two_layer_material(VX, VY, EToV, eps_right=2.25, x_interface=0.5):

@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 1
+#define DG_ABI_VERSION 2
 
 typedef struct dg_ctx dg_ctx;
 
@@ -85,12 +85,24 @@ typedef struct {
   const int32_t* part;   /* optional [K] element -> rank map; NULL = contiguous blocks
                             [r*K/P, (r+1)*K/P) of the input element order */
   void* stream;          /* cudaStream_t to enqueue on; NULL = the context creates its own */
+  /* ---- ABI 2 ---- */
+  int32_t max_ctas;      /* cap on the persistent stage kernels' grid (CTAs over the whole GPU);
+                            0 = every resident CTA (default).  A small cap makes each CTA walk many
+                            tiles through its shared-memory pipeline on a small mesh (slot reuse,
+                            mbarrier phase flips, next-tile prefetch): the parity tests use it to
+                            exercise at oracle size the code paths the full-size runs take. */
+  int32_t tile_order;    /* order in which each stage walks the tiles: 0 = first to last every stage
+                            (default); 1 = odd LSERK4 stages last to first.  Never changes a result. */
+  int32_t check_every;   /* 0 = off (default); S > 0: dg_run checks the fields for non-finite values
+                            after every S-th step on the device (one extra read of q), so dg_sync can
+                            report the first step found bad */
 } dg_options;
 
 /* Maximum N with compiled device kernels. */
 #define DG_MAX_KERNEL_N 9
 
-/* Fill *o with defaults: abi_version, N=4, fp64, device 0, alpha 1, rank 0 of 1, fused, NCCL. */
+/* Fill *o with defaults: abi_version, N=4, fp64, device 0, alpha 1, rank 0 of 1, fused, NCCL,
+ * max_ctas 0, tile_order 0, check_every 0. */
 dg_status dg_options_default(dg_options* o);
 
 /* Build a context (PAPER.md:139-198 problem statement; SURVEY.md §3 call stack 1).
@@ -112,10 +124,14 @@ dg_status dg_sizes(const dg_ctx* c, int64_t* Np, int64_t* Nfp, int64_t* K_local,
 /* Global element ids of the local elements, in local order [K_local]. */
 dg_status dg_local_elements(const dg_ctx* c, int64_t* gid);
 
-/* Upload fields (host fp64, canonical [K_local][Np]); resets the RK residual to 0. */
+/* Upload fields (fp64, canonical [K_local][Np]); resets the RK residual to 0.  Each pointer may be
+ * host memory (pageable or pinned) or device memory of this context's device (detected with
+ * cudaPointerGetAttributes; copied with cudaMemcpyDefault).  Enqueued on the context's stream;
+ * host sources are read before the call returns. */
 dg_status dg_set_fields(dg_ctx* c, const double* Hx, const double* Hy, const double* Ez);
 
-/* Download fields (host fp64, canonical [K_local][Np]); synchronises the context's stream. */
+/* Download fields (fp64, canonical [K_local][Np]) into host or device memory (as dg_set_fields);
+ * synchronises the context's stream. */
 dg_status dg_get_fields(dg_ctx* c, double* Hx, double* Hy, double* Ez);
 
 /* Advance nsteps LSERK4 steps of size dt (> 0): 5 stages per step, each one evaluation of the
@@ -124,20 +140,30 @@ dg_status dg_get_fields(dg_ctx* c, double* Hx, double* Hy, double* Ez);
 dg_status dg_run(dg_ctx* c, double dt, int64_t nsteps);
 
 /* Advance several in-process partitions (transport == 1 contexts of one mesh, ranks 0..n-1, all on
- * one device) in lock step; the halo exchange is a device-to-device copy.  Bitwise identical to a
- * single-partition run. */
+ * one device) in lock step; the halo exchange is a device-to-device copy.  Each fused stage runs as
+ * the NCCL path runs it: the interior tiles (no halo point) first, then the partition-boundary
+ * tiles (through the kernels' tile lists).  Bitwise identical to a single-partition run (SURVEY.md
+ * P17). */
 dg_status dg_run_group(dg_ctx* const* ctxs, int32_t n, double dt, int64_t nsteps);
 
-/* Synchronise the stream and check all fields for non-finite values (DG_E_DIVERGED). */
+/* Synchronise the stream and check all fields for non-finite values: DG_E_DIVERGED, with the
+ * step index in dg_last_error().  With options.check_every = S > 0 the message names the FIRST
+ * checked step at which a non-finite value appeared (exact for S = 1; for S > 1 the divergence
+ * happened within the S steps before it); with S = 0 it names the step count so far. */
 dg_status dg_sync(dg_ctx* c);
 
 /* Evaluate d/dt (Hx, Hy, Ez) of the current fields (host fp64 out, canonical [K_local][Np]);
  * which: 0 = full operator, 1 = volume term only (H2), 2 = surface term only (H3-H5). */
 dg_status dg_eval_rhs(dg_ctx* c, int32_t which, double* rHx, double* rHy, double* rEz);
 
-/* Discrete energy 1/2 sum_k J_k (mu_k H^T M H + eps_k Ez^T M Ez) of the local elements
- * (fp64 on the host from downloaded fields; the caller all-reduces across ranks). */
+/* Discrete energy 1/2 sum_k J_k (mu_k H^T M H + eps_k Ez^T M Ez) of the WHOLE mesh:
+ * fp64 on the host from downloaded fields, then, for an NCCL context (nranks > 1, transport 0),
+ * summed over the ranks with ncclAllReduce (every rank must call it; collective).  For in-process
+ * group contexts (transport 1) it is the local energy: sum dg_energy_local over the group. */
 dg_status dg_energy(dg_ctx* c, double* E);
+
+/* The same sum over this context's local elements only (no communication). */
+dg_status dg_energy_local(dg_ctx* c, double* E);
 
 /* ---- verification exports (host fp64, valid on host-only contexts) ---- */
 

@@ -49,8 +49,8 @@ struct StageArgs {
   int32_t ntiles;          // number of tiles to process (length of `tiles` if given)
   int32_t write_res;       // RK modes: store the residual (0 on the last stage)
   int32_t scale_volume;    // MODE_VOLUME with material: apply 1/mu, 1/eps (dg_eval_rhs only)
-  int32_t reverse;         // walk the tiles last to first (odd LSERK4 stages: the tiles the previous
-                           // stage wrote last are still in L2 and are read first)
+  int32_t reverse;         // walk the tiles last to first (dg_options.tile_order = 1: odd LSERK4 stages)
+  int32_t max_ctas;        // host only: cap on the persistent grid (0 = every resident CTA)
   double a, b, dt;         // LSERK4 stage coefficients and step
   double alpha;            // flux parameter (constant-material kernels)
 };

@@ -478,10 +478,14 @@ __device__ __forceinline__ void tmma(float (&c)[4], const uint32_t (&a)[4], uint
 }
 // x = hi + lo: hi = x rounded to nearest (ties away) at tf32's 10 mantissa bits by integer
 // add + mask -- the same rounding as cvt.rna.tf32 for finite x, without its NaN/Inf
-// handling (4 more instructions) -- and lo = x - hi, exact in fp32, read by the MMA as tf32
+// handling (4 more instructions) -- and lo = (x - hi) rounded the same way.  x - hi is exact
+// in fp32 but has up to 13 mantissa bits below tf32's; handing it to the MMA unrounded would
+// TRUNCATE it (a biased 2^-21 |x| error); rounded, |x - hi - lo| <= 2^-22 |x|, unbiased -- the
+// same treatment the host gives the operator's lo parts (pack_ops)
+__device__ __forceinline__ uint32_t rna_tf32(uint32_t u) { return (u + 0x1000u) & 0xFFFFE000u; }
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-  hi = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
-  lo = __float_as_uint(x - __uint_as_float(hi));
+  hi = rna_tf32(__float_as_uint(x));
+  lo = rna_tf32(__float_as_uint(x - __uint_as_float(hi)));
 }
 // c += A B with A = ah + al, B = bh + bl; the al bl term (~2^-22 relative) is dropped
 __device__ __forceinline__ void tmma3(float (&c)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], float bh0,
@@ -1214,7 +1218,8 @@ cudaError_t launch_one(const dg::StageArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     grid_cap[dev] = (per_sm > 0 ? per_sm : 1) * sms;
   }
-  const int grid = a.ntiles < grid_cap[dev] ? a.ntiles : grid_cap[dev];
+  int grid = a.ntiles < grid_cap[dev] ? a.ntiles : grid_cap[dev];
+  if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
   if (grid <= 0) return cudaSuccess;
   stage_kernel<MODE, MAT><<<grid, TEAM, smem, s>>>(a);
   return cudaGetLastError();

@@ -67,6 +67,7 @@ struct Nccl {
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -88,6 +89,7 @@ Nccl* nccl() {
   LOADSYM(GroupEnd, "ncclGroupEnd")
   LOADSYM(Send, "ncclSend")
   LOADSYM(Recv, "ncclRecv")
+  LOADSYM(AllReduce, "ncclAllReduce")
   LOADSYM(GetErrorString, "ncclGetErrorString")
 #undef LOADSYM
   n.ok = true;
@@ -152,6 +154,20 @@ __global__ void count_nonfinite(const T* __restrict__ q, int64_t n, int64_t fstr
   if (local) atomicAdd(bad, local);
 }
 
+// dg_options.check_every: the first checked step at which a field value is non-finite
+// (*first starts at ~0ull; non-finite values never become finite again under the scheme's
+// arithmetic, so the minimum over checks is the first bad check)
+template <typename T>
+__global__ void mark_nonfinite(const T* __restrict__ q, int64_t n, int64_t fstride, unsigned long long step,
+                               unsigned long long* first) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / n);
+    bad |= !isfinite(q[c * fstride + (i - c * n)]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMin(first, step);
+}
+
 int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -165,6 +181,7 @@ int grid_for(int64_t n) {
 struct dg_ctx {
   // options
   int N = 0, prec = 8, device = -1, rank = 0, nranks = 1, fused = 1, transport = 0;
+  int max_ctas = 0, tile_order = 0, check_every = 0;
   double alpha = 1.0;
   bool host_only = true, poisoned = false, material = false;
   // host setup
@@ -191,6 +208,8 @@ struct dg_ctx {
   void* sendbuf = nullptr;
   double* stage = nullptr;   // fp64 staging [3][Kl][Np]
   unsigned long long* flag = nullptr;
+  unsigned long long* first_bad = nullptr;  // check_every: first checked step with a non-finite value
+  double* ebuf = nullptr;                   // dg_energy all-reduce buffer
   int32_t* tiles_int = nullptr;
   int32_t* tiles_bnd = nullptr;
   int32_t n_int = 0, n_bnd = 0;
@@ -278,16 +297,6 @@ dg_status launch_stage(dg_ctx* c, int mode, const dg::StageArgs& a, cudaStream_t
   return DG_OK;
 }
 
-// Odd LSERK4 stages walk the tiles last to first (StageArgs::reverse); DG_REVERSE=0 disables it
-// (measurement A/B).  The order of tiles does not change any result.
-bool reverse_order() {
-  static const bool on = [] {
-    const char* e = std::getenv("DG_REVERSE");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 dg::StageArgs base_args(dg_ctx* c) {
   dg::StageArgs a{};
   a.q_in = c->q[c->cur];
@@ -305,6 +314,7 @@ dg::StageArgs base_args(dg_ctx* c) {
   a.write_res = 1;
   a.scale_volume = 0;
   a.alpha = c->alpha;
+  a.max_ctas = c->max_ctas;
   return a;
 }
 
@@ -349,42 +359,65 @@ dg_status exchange_nccl(dg_ctx* c, cudaStream_t s) {
   return DG_OK;
 }
 
-// One LSERK4 stage for a single (NCCL or single-rank) context.
-dg_status run_stage(dg_ctx* c, int i, double dt) {
+dg::StageArgs stage_args(dg_ctx* c, int i, double dt) {
   dg::StageArgs a = base_args(c);
   a.a = kRKa[i];
   a.b = kRKb[i];
   a.dt = dt;
   a.write_res = i == 4 ? 0 : 1;  // the residual is dead after the last stage (a_0 = 0)
-  a.reverse = (i & 1) && reverse_order();
-  const bool multi = c->nranks > 1 && c->transport == 0;
+  a.reverse = (i & 1) && c->tile_order == 1;
+  return a;
+}
+
+// The stage kernels of LSERK4 stage i of a partitioned context (nranks > 1) on stream s, the
+// same for both transports.  Fused: the interior tiles (no halo point) first, then -- after
+// halo_ready(), which makes s wait for the exchange -- the partition-boundary tiles, each
+// launch walking its tile list (StageArgs::tiles).  Split: the volume kernel (needs no halo),
+// halo_ready(), then the surface + RK kernel.
+template <typename WAIT>
+dg_status partitioned_stage(dg_ctx* c, const dg::StageArgs& a, cudaStream_t s, const WAIT& halo_ready) {
   dg_status st;
-  if (multi) {
+  if (c->fused) {
+    dg::StageArgs ai = a;
+    ai.tiles = c->tiles_int;
+    ai.ntiles = c->n_int;
+    if (ai.ntiles > 0 && (st = launch_stage(c, dg::MODE_FUSED_RK, ai, s, 0)) != DG_OK) return st;
+    if ((st = halo_ready()) != DG_OK) return st;
+    dg::StageArgs ab = a;
+    ab.tiles = c->tiles_bnd;
+    ab.ntiles = c->n_bnd;
+    if (ab.ntiles > 0 && (st = launch_stage(c, dg::MODE_FUSED_RK, ab, s, 0)) != DG_OK) return st;
+  } else {
+    dg::StageArgs av = a;
+    av.out = c->rhsv;  // the volume kernel's output is the surface kernel's rhsV input
+    if ((st = launch_stage(c, dg::MODE_VOLUME, av, s, 1)) != DG_OK) return st;
+    if ((st = halo_ready()) != DG_OK) return st;
+    if ((st = launch_stage(c, dg::MODE_SURFACE_RK, a, s, 2)) != DG_OK) return st;
+  }
+  return DG_OK;
+}
+
+// One LSERK4 stage for a single (NCCL or single-rank) context.
+dg_status run_stage(dg_ctx* c, int i, double dt) {
+  const dg::StageArgs a = stage_args(c, i, dt);
+  dg_status st;
+  if (c->nranks > 1 && c->transport == 0) {
     if ((st = pack(c, c->stream)) != DG_OK) return st;
     CU(c, cudaEventRecord(c->ev_pack, c->stream));
     CU(c, cudaStreamWaitEvent(c->comm, c->ev_pack, 0));
     if ((st = exchange_nccl(c, c->comm)) != DG_OK) return st;
     CU(c, cudaEventRecord(c->ev_comm, c->comm));
-  }
-  if (c->fused) {
-    if (multi) {
-      dg::StageArgs ai = a;
-      ai.tiles = c->tiles_int;
-      ai.ntiles = c->n_int;
-      if (ai.ntiles > 0 && (st = launch_stage(c, dg::MODE_FUSED_RK, ai, c->stream, 0)) != DG_OK) return st;
+    st = partitioned_stage(c, a, c->stream, [&]() -> dg_status {
       CU(c, cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
-      dg::StageArgs ab = a;
-      ab.tiles = c->tiles_bnd;
-      ab.ntiles = c->n_bnd;
-      if (ab.ntiles > 0 && (st = launch_stage(c, dg::MODE_FUSED_RK, ab, c->stream, 0)) != DG_OK) return st;
-    } else {
-      if ((st = launch_stage(c, dg::MODE_FUSED_RK, a, c->stream, 0)) != DG_OK) return st;
-    }
+      return DG_OK;
+    });
+    if (st != DG_OK) return st;
+  } else if (c->fused) {
+    if ((st = launch_stage(c, dg::MODE_FUSED_RK, a, c->stream, 0)) != DG_OK) return st;
   } else {
     dg::StageArgs av = a;
     av.out = c->rhsv;  // the volume kernel's output is the surface kernel's rhsV input
     if ((st = launch_stage(c, dg::MODE_VOLUME, av, c->stream, 1)) != DG_OK) return st;
-    if (multi) CU(c, cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
     if ((st = launch_stage(c, dg::MODE_SURFACE_RK, a, c->stream, 2)) != DG_OK) return st;
   }
   c->cur = 1 - c->cur;
@@ -521,6 +554,9 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
   if (!c->fused && (st = alloc(c, &c->rhsv, 3 * c->vstride * c->tsz)) != DG_OK) return st;
   if ((st = alloc(c, (void**)&c->stage, 3 * std::max<int64_t>(c->Kl * Np, 1) * sizeof(double))) != DG_OK) return st;
   if ((st = alloc(c, (void**)&c->flag, sizeof(unsigned long long))) != DG_OK) return st;
+  if ((st = alloc(c, (void**)&c->first_bad, sizeof(unsigned long long))) != DG_OK) return st;
+  if ((st = alloc(c, (void**)&c->ebuf, sizeof(double))) != DG_OK) return st;
+  CU(c, cudaMemset(c->first_bad, 0xff, sizeof(unsigned long long)));
   CU(c, cudaMemset(c->q[0], 0, 3 * c->fstride * c->tsz));
   CU(c, cudaMemset(c->q[1], 0, 3 * c->fstride * c->tsz));
   CU(c, cudaMemset(c->res, 0, 3 * c->vstride * c->tsz));
@@ -593,6 +629,20 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
   return DG_OK;
 }
 
+// A field pointer handed to dg_set_fields / dg_get_fields: host memory (pageable, pinned or
+// managed) or device memory of the context's own device; copies use cudaMemcpyDefault (UVA).
+dg_status check_field_ptr(dg_ctx* c, const void* p) {
+  cudaPointerAttributes at{};
+  const cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error of an unregistered pointer
+    return DG_OK;
+  }
+  if (at.type == cudaMemoryTypeDevice && at.device != c->device)
+    return set_err(DG_E_ARG, "field pointer is device memory of another device");
+  return DG_OK;
+}
+
 }  // namespace
 
 // ============================================================== C ABI
@@ -612,6 +662,9 @@ dg_status dg_options_default(dg_options* o) {
   o->nranks = 1;
   o->fused = 1;
   o->transport = 0;
+  o->max_ctas = 0;
+  o->tile_order = 0;
+  o->check_every = 0;
   return DG_OK;
 }
 
@@ -625,6 +678,8 @@ dg_status dg_setup(const dg_options* o, int64_t Nv, const double* VX, const doub
   if (o->nranks < 1 || o->rank < 0 || o->rank >= o->nranks) return set_err(DG_E_ARG, "bad rank / nranks");
   if (o->transport != 0 && o->transport != 1) return set_err(DG_E_ARG, "transport must be 0 or 1");
   if (!(o->alpha >= 0.0)) return set_err(DG_E_ARG, "alpha must be >= 0");
+  if (o->max_ctas < 0 || o->check_every < 0 || (o->tile_order != 0 && o->tile_order != 1))
+    return set_err(DG_E_ARG, "max_ctas and check_every must be >= 0, tile_order 0 or 1");
   if (eps)
     for (int64_t k = 0; k < K; ++k)
       if (!(eps[k] > 0.0) || !(mu[k] > 0.0)) return set_err(DG_E_ARG, "eps and mu must be > 0");
@@ -637,6 +692,9 @@ dg_status dg_setup(const dg_options* o, int64_t Nv, const double* VX, const doub
   c->nranks = o->nranks;
   c->fused = o->fused ? 1 : 0;
   c->transport = o->transport;
+  c->max_ctas = o->max_ctas;
+  c->tile_order = o->tile_order;
+  c->check_every = o->check_every;
   c->material = eps != nullptr;
   try {
     c->ref = dg::build_refelem(o->N);
@@ -693,7 +751,9 @@ dg_status dg_set_fields(dg_ctx* c, const double* Hx, const double* Hy, const dou
   const int64_t n = c->Kl * c->ref.Np;
   const double* src[3] = {Hx, Hy, Ez};
   for (int f = 0; f < 3; ++f)
-    CU(c, cudaMemcpyAsync(c->stage + f * n, src[f], n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if ((st = check_field_ptr(c, src[f])) != DG_OK) return st;
+  for (int f = 0; f < 3; ++f)
+    CU(c, cudaMemcpyAsync(c->stage + f * n, src[f], n * sizeof(double), cudaMemcpyDefault, c->stream));
   void* q = c->q[c->cur];
   if (c->tsz == 4)
     to_blocked<float><<<grid_for(3 * c->Kpad * c->ref.Np), 256, 0, c->stream>>>(
@@ -703,6 +763,8 @@ dg_status dg_set_fields(dg_ctx* c, const double* Hx, const double* Hy, const dou
         c->stage, (double*)q, c->perm_d, c->Kl, c->Kpad, c->ref.Np, c->fstride, c->km->swizzle);
   CU(c, cudaGetLastError());
   CU(c, cudaMemsetAsync(c->res, 0, 3 * c->vstride * c->tsz, c->stream));
+  CU(c, cudaMemsetAsync(c->first_bad, 0xff, sizeof(unsigned long long), c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));  // host sources are read before returning
   c->steps_done = 0;
   return DG_OK;
 }
@@ -723,10 +785,32 @@ dg_status dg_get_fields(dg_ctx* c, double* Hx, double* Hy, double* Ez) {
   CU(c, cudaGetLastError());
   double* dst[3] = {Hx, Hy, Ez};
   for (int f = 0; f < 3; ++f)
-    CU(c, cudaMemcpyAsync(dst[f], c->stage + f * n, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if ((st = check_field_ptr(c, dst[f])) != DG_OK) return st;
+  for (int f = 0; f < 3; ++f)
+    CU(c, cudaMemcpyAsync(dst[f], c->stage + f * n, n * sizeof(double), cudaMemcpyDefault, c->stream));
   CU(c, cudaStreamSynchronize(c->stream));
   return DG_OK;
 }
+
+}  // extern "C"
+
+namespace {
+dg_status check_step(dg_ctx* c) {  // options.check_every: mark the step if any value is non-finite
+  const int64_t n = c->Kpad * c->ref.Np;
+  const unsigned long long step = (unsigned long long)c->steps_done;
+  if (c->tsz == 4)
+    mark_nonfinite<float><<<grid_for(3 * n), 256, 0, c->stream>>>((const float*)c->q[c->cur], n, c->fstride, step,
+                                                                  c->first_bad);
+  else
+    mark_nonfinite<double><<<grid_for(3 * n), 256, 0, c->stream>>>((const double*)c->q[c->cur], n, c->fstride, step,
+                                                                   c->first_bad);
+  CU(c, cudaGetLastError());
+  c->stats.launches[3] += 1;
+  return DG_OK;
+}
+}  // namespace
+
+extern "C" {
 
 static void drop_graphs(dg_ctx* c) {
   for (int p = 0; p < 2; ++p) {
@@ -783,7 +867,9 @@ dg_status dg_run(dg_ctx* c, double dt, int64_t nsteps) {
   CU(c, cudaSetDevice(c->device));
   for (int64_t s = 0; s < nsteps; ++s) {
     // graph replay once a step has run eagerly (kernel attributes set up outside any capture)
-    if (c->graphs && c->nranks == 1 && c->steps_done > 0) {
+    // (NCCL contexts too: the pack, the comm-stream fork/join and the send/recv are captured; NCCL's
+    // peer connections were set up by the eager first step)
+    if (c->graphs && c->steps_done > 0) {
       if (c->gdt != dt) {
         drop_graphs(c);
         c->gdt = dt;
@@ -813,6 +899,7 @@ dg_status dg_run(dg_ctx* c, double dt, int64_t nsteps) {
         if ((st = run_stage(c, i, dt)) != DG_OK) return st;
     }
     ++c->steps_done;
+    if (c->check_every > 0 && c->steps_done % c->check_every == 0 && (st = check_step(c)) != DG_OK) return st;
   }
   return DG_OK;
 }
@@ -831,7 +918,7 @@ dg_status dg_set_graphs(dg_ctx* c, int32_t enable) {
 
 dg_status dg_run_group(dg_ctx* const* ctxs, int32_t n, double dt, int64_t nsteps) {
   if (!ctxs || n < 1) return set_err(DG_E_ARG, "empty group");
-  if (!(dt > 0.0) || nsteps < 0) return set_err(DG_E_ARG, "need dt > 0 and nsteps >= 0");
+  if (!(dt > 0.0) || !std::isfinite(dt) || nsteps < 0) return set_err(DG_E_ARG, "need dt > 0 and nsteps >= 0");
   std::vector<dg_ctx*> byrank(n, nullptr);
   for (int i = 0; i < n; ++i) {
     dg_status st = check_usable(ctxs[i], true);
@@ -866,21 +953,8 @@ dg_status dg_run_group(dg_ctx* const* ctxs, int32_t n, double dt, int64_t nsteps
                                   static_cast<const char*>(src->sendbuf) + (f * src->n_send + so) * src->tsz,
                                   cnt * c->tsz, cudaMemcpyDeviceToDevice, s));
         }
-      for (dg_ctx* c : byrank) {
-        dg::StageArgs a = base_args(c);
-        a.a = kRKa[i];
-        a.b = kRKb[i];
-        a.dt = dt;
-        a.write_res = i == 4 ? 0 : 1;
-        a.reverse = (i & 1) && reverse_order();
-        if (c->fused) {
-          if ((st = launch_stage(c, dg::MODE_FUSED_RK, a, s, 0)) != DG_OK) return st;
-        } else {
-          dg::StageArgs av = a;
-          av.out = c->rhsv;
-          if ((st = launch_stage(c, dg::MODE_VOLUME, av, s, 1)) != DG_OK) return st;
-          if ((st = launch_stage(c, dg::MODE_SURFACE_RK, a, s, 2)) != DG_OK) return st;
-        }
+      for (dg_ctx* c : byrank) {  // the NCCL path's launches; the copies above are already on s
+        if ((st = partitioned_stage(c, stage_args(c, i, dt), s, [] { return DG_OK; })) != DG_OK) return st;
         c->cur = 1 - c->cur;
       }
     }
@@ -903,9 +977,15 @@ dg_status dg_sync(dg_ctx* c) {
   else
     count_nonfinite<double><<<grid_for(3 * n), 256, 0, c->stream>>>((const double*)c->q[c->cur], n, c->fstride, c->flag);
   CU(c, cudaGetLastError());
-  unsigned long long bad = 0;
+  unsigned long long bad = 0, first = ~0ull;
   CU(c, cudaMemcpyAsync(&bad, c->flag, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
+  CU(c, cudaMemcpyAsync(&first, c->first_bad, sizeof(first), cudaMemcpyDeviceToHost, c->stream));
   CU(c, cudaStreamSynchronize(c->stream));
+  if (first != ~0ull)
+    return set_err(DG_E_DIVERGED, "non-finite field values first found at step " + std::to_string(first) +
+                                      " (checked every " + std::to_string(c->check_every) + " steps); " +
+                                      std::to_string(bad) + " non-finite values after step " +
+                                      std::to_string(c->steps_done));
   if (bad)
     return set_err(DG_E_DIVERGED, std::to_string(bad) + " non-finite field values after step " +
                                       std::to_string(c->steps_done));
@@ -943,7 +1023,7 @@ dg_status dg_eval_rhs(dg_ctx* c, int32_t which, double* rHx, double* rHy, double
   return DG_OK;
 }
 
-dg_status dg_energy(dg_ctx* c, double* E) {
+dg_status dg_energy_local(dg_ctx* c, double* E) {
   dg_status st = check_usable(c, true);
   if (st != DG_OK) return st;
   if (!E) return set_err(DG_E_ARG, "null output");
@@ -968,6 +1048,22 @@ dg_status dg_energy(dg_ctx* c, double* E) {
     tot += c->mesh.J[kl] * ek;
   }
   *E = 0.5 * tot;
+  return DG_OK;
+}
+
+dg_status dg_energy(dg_ctx* c, double* E) {
+  dg_status st = dg_energy_local(c, E);
+  if (st != DG_OK || c->nranks == 1 || c->transport != 0) return st;
+  Nccl* n = nccl();
+  if (!n || !c->nccl_comm) return set_err(DG_E_NCCL, "NCCL unavailable");
+  CU(c, cudaMemcpyAsync(c->ebuf, E, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  const ncclResult_t r = n->AllReduce(c->ebuf, c->ebuf, 1, ncclFloat64, ncclSum, c->nccl_comm, c->stream);
+  if (r != ncclSuccess) {
+    c->poisoned = true;
+    return set_err(DG_E_NCCL, std::string("ncclAllReduce: ") + n->GetErrorString(r));
+  }
+  CU(c, cudaMemcpyAsync(E, c->ebuf, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));
   return DG_OK;
 }
 
@@ -1106,7 +1202,8 @@ void dg_destroy(dg_ctx* c) {
       if (n) (c->poisoned ? n->CommAbort : n->CommDestroy)(c->nccl_comm);
     }
     void* bufs[] = {c->q[0], c->q[1], c->res, c->rhsv, c->out, c->geo, c->ops, c->vmapP, c->send_idx,
-                    c->sendbuf, c->stage, c->flag, c->tiles_int, c->tiles_bnd, c->perm_d, c->slot_of_d};
+                    c->sendbuf, c->stage, c->flag, c->first_bad, c->ebuf, c->tiles_int, c->tiles_bnd,
+                    c->perm_d, c->slot_of_d};
     for (void* b : bufs)
       if (b) cudaFree(b);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

@@ -22,7 +22,7 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built; run `python -m paper_1304_5546_b200.build`")
 _lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_KERNEL_N = 9
 
 STATUS = {0: "DG_OK", 1: "DG_E_ARG", 2: "DG_E_DEGREE", 3: "DG_E_MESH_DEGENERATE",
@@ -30,7 +30,7 @@ STATUS = {0: "DG_OK", 1: "DG_E_ARG", 2: "DG_E_DEGREE", 3: "DG_E_MESH_DEGENERATE"
           7: "DG_E_CUDA", 8: "DG_E_NCCL", 9: "DG_E_OOM", 10: "DG_E_DIVERGED", 11: "DG_E_STATE"}
 
 EXPORTS = ["dg_options_default", "dg_setup", "dg_sizes", "dg_local_elements", "dg_set_fields",
-           "dg_get_fields", "dg_run", "dg_run_group", "dg_sync", "dg_eval_rhs", "dg_energy",
+           "dg_get_fields", "dg_run", "dg_run_group", "dg_sync", "dg_eval_rhs", "dg_energy", "dg_energy_local",
            "dg_get_operators", "dg_get_geometry", "dg_get_maps", "dg_get_nodes", "dg_halo_sizes",
            "dg_get_halo", "dg_stream", "dg_profile", "dg_get_kernel_stats", "dg_get_kernel_config", "dg_set_graphs",
            "dg_destroy", "dg_last_error"]
@@ -47,7 +47,8 @@ class Options(C.Structure):
     _fields_ = [("abi_version", C.c_int32), ("N", C.c_int32), ("precision", C.c_int32),
                 ("device", C.c_int32), ("alpha", C.c_double), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("fused", C.c_int32), ("transport", C.c_int32),
-                ("nccl_id", C.c_void_p), ("part", C.c_void_p), ("stream", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("part", C.c_void_p), ("stream", C.c_void_p),
+                ("max_ctas", C.c_int32), ("tile_order", C.c_int32), ("check_every", C.c_int32)]
 
 
 class KernelStats(C.Structure):
@@ -80,6 +81,7 @@ _sig = {
     "dg_sync": [_vp],
     "dg_eval_rhs": [_vp, C.c_int32, _vp, _vp, _vp],
     "dg_energy": [_vp, _vp],
+    "dg_energy_local": [_vp, _vp],
     "dg_get_operators": [_vp] * 7,
     "dg_get_geometry": [_vp] * 10,
     "dg_get_maps": [_vp] * 5,
@@ -172,14 +174,25 @@ class Context:
         return self._h
 
     # -- fields
-    def _fields_in(self, fields):
+    def _fields_io(self, fields, writable=False):
+        """Validate field buffers: numpy arrays (converted to contiguous fp64 on input) or torch
+        tensors (fp64, contiguous, CPU or this context's CUDA device -- dg_set_fields /
+        dg_get_fields copy with cudaMemcpyDefault), each of K_local * Np values."""
         n = self.K_local * self.Np
         out = []
         for a in fields:
             if isinstance(a, np.ndarray):
-                a = _as(a, np.float64, n)
-            elif a.numel() != n:
-                raise ValueError("field size mismatch")
+                if writable:
+                    if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"] or a.size != n \
+                            or not a.flags["WRITEABLE"]:
+                        raise ValueError(f"output arrays must be writable C-contiguous float64 of {n} values")
+                else:
+                    a = _as(a, np.float64, n)
+            else:  # torch tensor
+                if str(a.dtype) != "torch.float64" or not a.is_contiguous() or a.numel() != n:
+                    raise ValueError(f"field tensors must be contiguous torch.float64 of {n} values")
+                if a.device.type not in ("cpu", "cuda"):
+                    raise ValueError(f"unsupported tensor device {a.device}")
             out.append(a)
         return out
 
@@ -189,12 +202,13 @@ class Context:
         return g
 
     def set_fields(self, Hx, Hy, Ez):
-        a = self._fields_in((Hx, Hy, Ez))
+        a = self._fields_io((Hx, Hy, Ez))
         _check(_lib.dg_set_fields(self._h, _ptr(a[0]), _ptr(a[1]), _ptr(a[2])))
 
     def get_fields(self, out=None):
         if out is None:
             out = tuple(np.empty((self.K_local, self.Np)) for _ in range(3))
+        self._fields_io(out, writable=True)
         _check(_lib.dg_get_fields(self._h, _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
         return out
 
@@ -211,8 +225,15 @@ class Context:
         return out
 
     def energy(self):
+        """dg_energy: the whole mesh's energy (all-reduced over an NCCL communicator: collective)."""
         e = C.c_double()
         _check(_lib.dg_energy(self._h, C.byref(e)))
+        return e.value
+
+    def energy_local(self):
+        """dg_energy_local: this partition's share of the energy (no communication)."""
+        e = C.c_double()
+        _check(_lib.dg_energy_local(self._h, C.byref(e)))
         return e.value
 
     # -- verification exports
@@ -290,7 +311,8 @@ class Context:
 
 
 def dg_setup(N, VX, VY, EToV, eps=None, mu=None, bctag=None, precision=8, device=0, alpha=1.0,
-             rank=0, nranks=1, fused=True, transport=0, nccl_id=None, part=None, stream=None):
+             rank=0, nranks=1, fused=True, transport=0, nccl_id=None, part=None, stream=None,
+             max_ctas=0, tile_order=0, check_every=0):
     """dg_setup: build a context for ``rank`` of ``nranks`` on the GLOBAL mesh (VX, VY, EToV)."""
     VX = _as(VX, np.float64)
     VY = _as(VY, np.float64)
@@ -311,6 +333,7 @@ def dg_setup(N, VX, VY, EToV, eps=None, mu=None, bctag=None, precision=8, device
         o.nccl_id = C.cast(idbuf, C.c_void_p)
     o.part = _ptr(part_a)
     o.stream = stream
+    o.max_ctas, o.tile_order, o.check_every = int(max_ctas), int(tile_order), int(check_every)
     h = C.c_void_p()
     _check(_lib.dg_setup(C.byref(o), VX.size, _ptr(VX), _ptr(VY), K, _ptr(EToV), _ptr(eps_a), _ptr(mu_a),
                          _ptr(bc_a), C.byref(h)))

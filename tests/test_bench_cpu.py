@@ -47,3 +47,46 @@ def test_algorithmic_bytes_and_flops_hand_counts():
     assert bench.flops_per_element_stage(5) == 8 * 441 + 8 * 21 + 18 * 21 * 6 + 108 * 6 + 12 * 21 == 6864
     assert bench.flops_per_element_stage(5, "volume") + bench.flops_per_element_stage(5, "surface") \
         == 6864 + 3 * 21
+
+
+def test_spawn_ranks_builds_torchrun_command(monkeypatch):
+    seen = {}
+
+    def fake_execv(exe, cmd):
+        seen["cmd"] = cmd
+        raise SystemExit(0)
+
+    monkeypatch.setattr(os, "execv", fake_execv)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    try:
+        bench.spawn_ranks(4)
+    except SystemExit:
+        pass
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--nnodes=1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"]
+
+
+def test_physical_gpu_follows_cuda_visible_devices(monkeypatch):
+    monkeypatch.setenv("CUDA_VISIBLE_DEVICES", "3,5")
+    assert bench.physical_gpu(1) == "5"
+    monkeypatch.setenv("CUDA_VISIBLE_DEVICES", "GPU-abc,GPU-def")
+    assert bench.physical_gpu(0) == "GPU-abc"
+    monkeypatch.delenv("CUDA_VISIBLE_DEVICES")
+    assert bench.physical_gpu(2) == "2"
+
+
+def test_clock_summary_keeps_the_timed_window():
+    c = bench.ClockSampler("0")
+    c.samples = [(0.0, 900.0, 1965.0, []), (1.0, 1965.0, 1965.0, ["sw_power_cap"]),
+                 (2.0, 1965.0, 1965.0, []), (3.0, 120.0, 1965.0, ["hw_slowdown"])]
+    s = c.summary(0.5, 2.5)
+    assert s["sm_mhz"] == 1965.0 and s["reasons"] == ["sw_power_cap"] and s["samples_in_timed_region"] == 2
+
+
+def test_cpu_baseline_all_cores_and_single_thread():
+    cb = bench.cpu_baseline(2, 3, 2)
+    assert cb["kind"] == "oracle" and cb["cores"] == (os.cpu_count() or 1) and cb["value"] > 0
+    assert cb["single_thread"]["cores"] == 1 and cb["single_thread"]["value"] > 0
+    assert "3x3" in cb["sample"]

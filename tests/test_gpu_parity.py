@@ -37,8 +37,8 @@ def relerr(a, b):
     return max(float(np.abs(x - y).max() / max(np.abs(y).max(), 1e-300)) for x, y in zip(a, b))
 
 
-def _initial(o, amp=1e-3, seed=dginputs.SEED, mode=(1, 1)):
-    q = dginputs.cavity_mode(o.geo.x, o.geo.y, 0.0, *mode)
+def _initial(o, amp=1e-3, seed=dginputs.SEED, mode=(1, 1), t0=0.0):
+    q = dginputs.cavity_mode(o.geo.x, o.geo.y, t0, *mode)
     p = dginputs.perturbation(o.geo.x.shape, amp, seed)
     return tuple(a + b for a, b in zip(q, p))
 
@@ -109,9 +109,12 @@ def test_c1_100_steps(prec, fused):
 def test_order_sweep_run(N, prec):
     VX, VY, E = _jittered(9, seed=N)      # K = 162: 6 tiles, ragged tail
     o = Oracle(N, VX, VY, E)
-    q0 = _initial(o, amp=1e-2)
+    # the (1,1) mode at phase pi/4: every field O(1), so the per-field A14 quotient is well
+    # conditioned (at t0 = 0, H is only the 1e-2 perturbation and its quotient measures Ez's
+    # rounding against H's small scale: N=8 fp64 1.3e-12 at 100 steps)
+    q0 = _initial(o, amp=1e-2, t0=dginputs.C4_T0)
     dt = dginputs.cfl_dt(VX, VY, o.EToV, N)
-    nsteps = 100 if N <= 6 else 40
+    nsteps = 100
     want = o.run(q0, dt, nsteps)
     c = dg.dg_setup(N, VX, VY, E, precision=prec)
     c.set_fields(*q0)
@@ -141,10 +144,13 @@ def test_two_layer_material_run(prec):
     c.destroy()
 
 
+@pytest.mark.parametrize("order", [0, 1])
 @pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("P", [2, 3, 5])
-def test_partitioned_group_bitwise_equals_single(P, fused):
-    # P partitions (same kernels + halo exchange) == 1 partition, bitwise
+def test_partitioned_group_bitwise_equals_single(P, fused, order):
+    # P partitions (same kernels + halo exchange) == 1 partition, bitwise.  Each fused
+    # stage of a partition runs as the NCCL path runs it: interior tiles, then boundary tiles, both
+    # through the kernels' tile lists (StageArgs::tiles); both tile orders, a capped grid.
     N = 5
     VX, VY, E = _jittered(10, seed=P)
     eps, mu = dginputs.two_layer_material(VX, VY, E)
@@ -159,7 +165,8 @@ def test_partitioned_group_bitwise_equals_single(P, fused):
     rng = np.random.default_rng(P)
     part = rng.integers(0, P, E.shape[0]).astype(np.int32) if P == 5 else None
     cs = [dg.dg_setup(N, VX, VY, E, eps=eps, mu=mu, precision=8, fused=fused, rank=r, nranks=P,
-                      transport=1, part=part) for r in range(P)]
+                      transport=1, part=part, tile_order=order, max_ctas=2 if order else 0)
+          for r in range(P)]
     for c in cs:
         gid = c.local_elements()
         c.set_fields(*(a[gid] for a in q0))
@@ -260,7 +267,7 @@ def c4():
     VX, VY, E = dginputs.rect_mesh(n)
     c = dg.dg_setup(5, VX, VY, E, precision=4)
     x, y = c.nodes()
-    q0 = dginputs.cavity_mode(x, y, 0.0)
+    q0 = dginputs.cavity_mode(x, y, dginputs.C4_T0)
     q0 = tuple(a + b for a, b in zip(q0, dginputs.perturbation(x.shape, 1e-3)))
     yield dict(c=c, VX=VX, VY=VY, E=E, n=n, q0=q0)
     c.destroy()
@@ -307,16 +314,17 @@ C4_GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "c4_oracle_100step
 @pytest.mark.skipif(not os.path.exists(C4_GOLDEN), reason="tools/make_c4_golden.py not run")
 @pytest.mark.parametrize("prec", [4, 8])
 def test_c4_full_size_100_steps_vs_oracle(c4, prec):
-    """The bench workload exactly (C4, fused, 100 steps; fp32 = the bench's dtype) against the
-    fp64 oracle run on the WHOLE mesh (tests/golden/c4_oracle_100steps_sampled.npz, written by
-    tools/make_c4_golden.py from oracle/ only), on the stored sample of elements.
+    """The bench workload exactly (C4: N=5, K=1,048,352, fused, 100 steps, the bench's launch
+    configuration; fp32 = the bench's dtype) against the fp64 oracle run on the WHOLE mesh
+    (tests/golden/c4_oracle_100steps_sampled.npz, written by tools/make_c4_golden.py from oracle/
+    only), on the stored sample of 4,100 elements.
 
-    Metric (reading A14'): max_F max|F_gpu - F_orc| / max_F max|F_orc|, the error
-    relative to the state's scale.  The per-field A14 form is ill-conditioned here: the cavity
-    mode's H starts at 0 and is only 0.028 after 100 steps while the rounding error of the
-    discrete curl scales with Ez (1.0) / h; the per-field values are reported, not asserted."""
+    Metric: SURVEY A14 per field, max|F_gpu - F_orc| / max|F_orc| for each of Hx, Hy, Ez, on a
+    well-conditioned input -- the (1,1) mode at phase w t0 = pi/4, where every field is O(1)
+    (DESIGN.md §2 A14)."""
     gold = np.load(C4_GOLDEN)
     assert int(gold["N"]) == 5 and int(gold["n"]) == c4["n"] and int(gold["steps"]) == 100
+    assert float(gold["t0"]) == dginputs.C4_T0
     dt = float(gold["dt"])
     assert dt == dginputs.cfl_dt(c4["VX"], c4["VY"], c4["E"], 5)
     c = c4["c"] if prec == 4 else dg.dg_setup(5, c4["VX"], c4["VY"], c4["E"], precision=8)
@@ -329,9 +337,8 @@ def test_c4_full_size_100_steps_vs_oracle(c4, prec):
     names = ("Hx", "Hy", "Ez")
     abserr = [float(np.abs(got[F][el] - gold[nm]).max()) for F, nm in enumerate(names)]
     per_field = [e / float(m) for e, m in zip(abserr, gold["maxabs"])]
-    state = max(abserr) / float(gold["maxabs"].max())
-    print(f"C4 prec={prec}: state-relative {state:.3e}, per-field {per_field}")
-    assert state <= TOL_RUN[prec], (state, per_field)
+    print(f"C4 prec={prec}: per-field A14 {['%.3e' % e for e in per_field]}")
+    assert max(per_field) <= TOL_RUN[prec], per_field
 
 
 def test_c4_full_size_100_steps_properties(c4):

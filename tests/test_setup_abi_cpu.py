@@ -175,3 +175,34 @@ def test_large_mesh_setup_is_fast_and_consistent():
             mine = h["recv_gdof"][h["recv_off"][t_]:h["recv_off"][t_ + 1]]
             theirs = hp["send_gdof"][hp["send_off"][u]:hp["send_off"][u + 1]]
             assert np.array_equal(mine, theirs)
+
+
+def test_field_buffers_are_validated_before_the_call():
+    """dg.py checks dtype / contiguity / size of field buffers (numpy and torch) before handing raw
+    pointers to dg_set_fields / dg_get_fields (host-only context: the C call is never reached)."""
+    import torch
+
+    VX, VY, E = dginputs.rect_mesh(2)
+    c = dg.dg_setup(3, VX, VY, E, device=-1)
+    n = c.K_local * c.Np
+    with pytest.raises(ValueError):
+        c.set_fields(*(torch.zeros(n, dtype=torch.float32) for _ in range(3)))
+    with pytest.raises(ValueError):
+        c.set_fields(*(torch.zeros(2 * n, dtype=torch.float64)[::2] for _ in range(3)))
+    with pytest.raises(ValueError):
+        c.get_fields(tuple(np.empty(n, dtype=np.float32) for _ in range(3)))
+    with pytest.raises(ValueError):
+        c.get_fields(tuple(np.empty(n + 1) for _ in range(3)))
+    with pytest.raises(dg.DGError) as e:  # well-formed buffers reach the library: host-only context
+        c.set_fields(*(np.zeros(n) for _ in range(3)))
+    assert e.value.name == "DG_E_STATE"
+    c.destroy()
+
+
+def test_abi2_options_are_validated():
+    VX, VY, E = dginputs.rect_mesh(2)
+    for kw in (dict(max_ctas=-1), dict(check_every=-2), dict(tile_order=2)):
+        with pytest.raises(dg.DGError) as e:
+            dg.dg_setup(3, VX, VY, E, device=-1, **kw)
+        assert e.value.name == "DG_E_ARG"
+    dg.dg_setup(3, VX, VY, E, device=-1, max_ctas=3, tile_order=1, check_every=5).destroy()

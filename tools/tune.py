@@ -8,8 +8,12 @@
 
 Knobs: R (max rows per warp -> team size), S (shared-memory slots), C (teams/SM cap).
 Timing: one LSERK4 stage = one fused launch, CUDA events, mean of 5 steps after warm-up,
-on an n x n A16 mesh (default n=362, K=262,088).  Every variant's result is checked
-against the default build's fields after the run (identical arithmetic => bitwise).
+on an n x n A16 mesh (default n=362, K=262,088).  Oracle gate ("every timed variant
+passes the oracle gate"): each variant also runs 100 steps of every (N, precision) on the jittered
+12x12 mesh with the grid capped at 2 CTAs (each CTA walks 4-5 tiles: the full-size pipeline) and
+is compared field by field with the fp64 oracle's fields stored in tests/golden/pipeline_gate_n12.npz
+(tools/make_pipeline_gate_golden.py); `pick` disqualifies any variant whose per-field A14 error
+exceeds 1e-12 (fp64) / 2e-5 (fp32).
 """
 import itertools
 import json
@@ -89,6 +93,7 @@ import sys, json; sys.path.insert(0, {ROOT!r})
 import numpy as np, torch, dginputs
 from paper_1304_5546_b200 import dg
 VX, VY, E = dginputs.rect_mesh({n})
+G = np.load({os.path.join(ROOT, "tests", "golden", "pipeline_gate_n12.npz")!r})
 out = []
 for N in range(1, 10):
     dt = dginputs.cfl_dt(VX, VY, E, N)
@@ -105,8 +110,16 @@ for N in range(1, 10):
         e0.record(s); c.run(dt, 5); e1.record(s); e1.synchronize()
         ms = e0.elapsed_time(e1) / 25
         f = c.get_fields()
-        out.append(dict(N=N, prec=prec, ms=ms, chk=float(sum(np.abs(a).sum() for a in f))))
         c.destroy()
+        # oracle gate: 100 steps on the stored case, grid capped (multi-tile pipeline), per-field A14
+        g = c = dg.dg_setup(N, G["VX"], G["VY"], G["EToV"], precision=prec, max_ctas=2)
+        xg, yg = g.nodes()
+        q0 = dginputs.cavity_mode(xg, yg, float(G["t0"]))
+        q0 = tuple(a + b for a, b in zip(q0, dginputs.perturbation(xg.shape, float(G["amplitude"]), seed=N)))
+        g.set_fields(*q0); g.run(float(G["dt%d" % N]), int(G["steps"])); got = g.get_fields(); g.destroy()
+        gate = max(float(np.abs(a - G[nm + str(N)]).max() / np.abs(G[nm + str(N)]).max())
+                   for a, nm in zip(got, ("Hx", "Hy", "Ez")))
+        out.append(dict(N=N, prec=prec, ms=ms, chk=float(sum(np.abs(a).sum() for a in f)), gate=gate))
 print(json.dumps(out))
 """
         env = dict(os.environ, DG_LIB=os.path.join(VDIR, lib))
@@ -135,6 +148,10 @@ def cmd_pick(*paths):
     chk = {}
     for r in d["results"]:
         key = f"N{r['N']}_{'f32' if r['prec'] == 4 else 'f64'}"
+        tol = 1e-12 if r["prec"] == 8 else 2e-5
+        if "gate" not in r or not r["gate"] <= tol:
+            print("DISQUALIFIED (oracle gate)", key, r["variant"], r.get("gate", "not run"))
+            continue
         chk.setdefault(key, r["chk"])
         if abs(r["chk"] - chk[key]) > 1e-6 * abs(chk[key]):
             print("WARNING: checksum mismatch", key, r["variant"])
