@@ -27,6 +27,15 @@ SEED = 20261017
 C4_T0 = 0.25 / math.sqrt(2.0)
 
 
+def balanced_start(T, m=1, n=1):
+    """Start time t0 of the exact cavity mode (m, n) such that the state at the END of a run of length
+    T has phase w (t0 + T) = pi/4: every field is O(1) where a parity test measures it, so the per-field
+    A14 quotient is well conditioned (DESIGN.md §2 A14).  t0 may be negative (the exact mode is valid
+    for every t)."""
+    w = math.pi * math.sqrt(m * m + n * n)
+    return math.pi / (4.0 * w) - T
+
+
 # ----------------------------------------------------------------------------
 # Mesh (SURVEY.md §8(c) A16, SPEC.md:139-147)
 # ----------------------------------------------------------------------------

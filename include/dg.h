@@ -96,13 +96,16 @@ typedef struct {
   int32_t check_every;   /* 0 = off (default); S > 0: dg_run checks the fields for non-finite values
                             after every S-th step on the device (one extra read of q), so dg_sync can
                             report the first step found bad */
+  int32_t kernel_variant; /* 0 = the stage kernels tuned for this (N, precision) (default; see
+                             dg_get_kernel_config); 1 = fp32 only: the tcgen05 kernels (5th-generation
+                             tensor cores, TMEM accumulators, 128-element groups) */
 } dg_options;
 
 /* Maximum N with compiled device kernels. */
 #define DG_MAX_KERNEL_N 9
 
 /* Fill *o with defaults: abi_version, N=4, fp64, device 0, alpha 1, rank 0 of 1, fused, NCCL,
- * max_ctas 0, tile_order 0, check_every 0. */
+ * max_ctas 0, tile_order 0, check_every 0, kernel_variant 0. */
 dg_status dg_options_default(dg_options* o);
 
 /* Build a context (PAPER.md:139-198 problem statement; SURVEY.md §3 call stack 1).
@@ -227,7 +230,9 @@ typedef struct {
   int32_t contraction;   /* volume + LIFT contractions: 0 = CUDA-core FMA (FFMA/DFMA),
                             1 = fp64 tensor cores (DMMA, mma.sync m8n8k4),
                             2 = fp32 on tensor cores as 3xTF32 (mma.sync m16n8k8; each operand
-                                split hi + lo, hi*hi + lo*hi + hi*lo in fp32 accumulation) */
+                                split hi + lo, hi*hi + lo*hi + hi*lo in fp32 accumulation),
+                            3 = fp32 as 3xTF32 on the 5th-generation tensor cores (tcgen05.mma
+                                kind::tf32, M = 128 elements, A operands and accumulators in TMEM) */
   int32_t threads;       /* threads per CTA; one CTA owns one 32-element tile at a time */
   int32_t slots;         /* shared-memory pipeline slots (1 or 2) */
   int32_t residual_tma;  /* 1: the LSERK4 residual is staged into shared memory by TMA */

@@ -42,11 +42,11 @@ struct StageArgs {
   void* out;               // [3][vstride] T   (MODE_VOLUME / MODE_RHS / MODE_SURFACE)
   const void* geo;         // [ntiles][NGEO][32] T
   const int32_t* vmapP;    // [ntiles][3 Nfp][32] offsets into a field (tile-blocked or ghost)
-  const int32_t* tiles;    // optional list of tile ids to process (NULL: 0..ntiles-1)
+  const int32_t* tiles;    // optional list of tile (group) ids to process (NULL: 0..ntiles-1)
   const void* ops;         // packed operators (KernelModule::pack_ops layout), device memory
   int64_t fstride;         // elements between fields of q (local + ghosts)
   int64_t vstride;         // elements between fields of res / rhsv / out
-  int32_t ntiles;          // number of tiles to process (length of `tiles` if given)
+  int32_t ntiles;          // number of tiles (groups, KernelModule::tile_group) to process
   int32_t write_res;       // RK modes: store the residual (0 on the last stage)
   int32_t scale_volume;    // MODE_VOLUME with material: apply 1/mu, 1/eps (dg_eval_rhs only)
   int32_t reverse;         // walk the tiles last to first (dg_options.tile_order = 1: odd LSERK4 stages)
@@ -59,7 +59,7 @@ struct KernelInfo {
   int N, prec;                       // prec = 4 or 8
   int threads, slots, row_groups, rows_per_group;
   size_t smem_bytes;
-  int contraction;   // 0 FMA, 1 fp64 DMMA, 2 fp32 3xTF32 (dg.h dg_kernel_config)
+  int contraction;   // 0 FMA, 1 fp64 DMMA, 2 fp32 3xTF32 mma.sync, 3 fp32 3xTF32 tcgen05 (dg.h)
   int residual_tma;  // LSERK4 residual staged by TMA
   int teams_cap;     // DG_C
   int flags;         // bit 0 DG_FF (flux first), bit 1 DG_OG (operators via L1), bit 2 DG_FX, bit 3 DG_IL
@@ -79,6 +79,13 @@ struct KernelModule {
   // column swizzle of the tile-blocked layout: element `lane` of node row n lives at
   // column swz_col(swizzle, n, lane) (0 = plain layout)
   int swizzle = 0;
+  // tiles per work unit: the stage kernels walk groups of tile_group consecutive tiles (4 for the
+  // tcgen05 kernels: M = 128 elements); StageArgs::ntiles and ::tiles count and list GROUPS, and
+  // a neighbour in the same group is read from shared memory (vmapP code < 0)
+  int tile_group = 1;
+  // 0: the tuned module of this (N, precision) (csrc/tune.json); 1: the tcgen05 variant module
+  // (fp32 only; dg_options.kernel_variant = 1)
+  int variant = 0;
 };
 
 // Column of element e (0..31) of node row n in the tile-blocked layout, swizzle mode swm:
@@ -93,6 +100,6 @@ __host__ __device__ constexpr int swz_col(int swm, int n, int e) {
 }
 
 // Registry: one entry per compiled (N, prec); nullptr if not compiled.
-const KernelModule* find_module(int N, int prec);
+const KernelModule* find_module(int N, int prec, int variant = 0);
 
 }  // namespace dg

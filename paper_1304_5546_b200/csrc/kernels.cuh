@@ -32,6 +32,8 @@
 //   C  lift:    rhs += LIFT f
 //   D  update:  res = a res + dt rhs;  q_out = q_in + b res
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -65,12 +67,18 @@ constexpr int TL = dg::TILE;
 #ifndef DG_MMA
 #define DG_MMA 0  // chosen per (N, precision) by tools/tune.py
 #endif
-constexpr bool USE_MMA = !F32 && DG_MMA;
+constexpr bool USE_MMA = !F32 && (DG_MMA == 1 || DG_MMA == 2);
 // fp32 only: the same contractions as 3xTF32 products on the tensor cores (mma.sync
 // m16n8k8: A = fields, elements x nodes; B = operator^T), split hi + lo so the result
 // keeps fp32 accuracy -- DG_MMA=1: one 16-element m-tile per warp, two warps per tile;
 // DG_MMA=2: four warps, each an m-tile x one field set (Hx, Hy | Ez)
-constexpr bool USE_TF = F32 && DG_MMA;
+constexpr bool USE_TF = F32 && (DG_MMA == 1 || DG_MMA == 2);
+// fp32 only, DG_MMA=3: the contractions on the 5th-generation tensor cores (tcgen05.mma kind::tf32,
+// accumulators and A operands in TMEM), 3xTF32 split; 128-element groups (kernels_tc.cuh)
+constexpr bool USE_TC = F32 && DG_MMA == 3;
+#ifndef DG_VARIANT
+#define DG_VARIANT 0  // 0: the tuned module of this (N, precision); 1: the tcgen05 variant module
+#endif
 constexpr bool TF_SPLIT = USE_TF && DG_MMA == 2;  // 4 warps: m-tile x {Hx, Hy | Ez}
 constexpr bool DMMA_SPLIT = USE_MMA && DG_MMA == 2;  // 2 PR warps: row group x {Hx, Hy | Ez}
 constexpr int PR = (NP + 7) / 8;                     // DMMA row groups (8 output rows each)
@@ -129,7 +137,7 @@ __device__ __forceinline__ V ldop(const V* p) {
 // column swz_col(SWM, n, e) (kernel_api.h).  Identity for the FMA kernels; for the DMMA kernels
 // it makes the B-fragment loads (4 rows x 8 elements) bank-conflict free, for the
 // TF32 kernels the A-fragment loads (8 elements x 4 nodes).
-constexpr int SWM = USE_MMA ? 4 : (USE_TF ? 8 : 0);
+constexpr int SWM = USE_MMA ? 4 : (USE_TF ? 8 : 0);  // identity for the FMA and tcgen05 kernels
 __host__ __device__ constexpr int colx(int n, int e) { return dg::swz_col(SWM, n, e); }
 constexpr size_t QB = (size_t)3 * NP * TL * sizeof(T);
 __host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)(mat ? dg::NGEO_MAT : dg::NGEO_CONST) * TL * sizeof(T); }
@@ -1199,8 +1207,13 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   }
 }
 
+#include "kernels_tc.cuh"
+
 template <int MODE, bool MAT>
 cudaError_t launch_one(const dg::StageArgs& a, cudaStream_t s) {
+  if constexpr (USE_TC) {
+    return tc::launch_one<MODE, MAT>(a, s);
+  } else {
   using MT = ModeTraits<MODE>;
   constexpr size_t smem = smem_total(nslots(MT::surf, MAT), MT::surf, MAT, MT::rk);
   static int grid_cap[64] = {0};  // resident CTAs (whole GPU) per device ordinal
@@ -1210,7 +1223,7 @@ cudaError_t launch_one(const dg::StageArgs& a, cudaStream_t s) {
   if (dev >= 64) return cudaErrorInvalidDevice;
   if (grid_cap[dev] == 0) {
     e = cudaFuncSetAttribute(stage_kernel<MODE, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) return cudaGetLastError(), e;
     int per_sm = 0, sms = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_kernel<MODE, MAT>, TEAM, smem);
     if (e != cudaSuccess) return e;
@@ -1223,6 +1236,7 @@ cudaError_t launch_one(const dg::StageArgs& a, cudaStream_t s) {
   if (grid <= 0) return cudaSuccess;
   stage_kernel<MODE, MAT><<<grid, TEAM, smem, s>>>(a);
   return cudaGetLastError();
+  }
 }
 
 cudaError_t launch(int mode, bool mat, const dg::StageArgs& a, cudaStream_t s) {
@@ -1249,9 +1263,13 @@ cudaError_t launch(int mode, bool mat, const dg::StageArgs& a, cudaStream_t s) {
 // Host: pack Dr, Ds [Np][Np] and LIFT [Np][3Nfp] (fp64, row-major) into the
 // kernels' shared-memory operator layout (rounded once to T; padded rows and
 // columns are zero).
-size_t ops_bytes() { return OPB; }
+size_t ops_bytes() { return USE_TC ? tc::OPS : OPB; }
 void pack_ops(const double* Dr, const double* Ds, const double* LIFT, void* out) {
   unsigned char* o = static_cast<unsigned char*>(out);
+  if constexpr (USE_TC) {
+    tc::pack(Dr, Ds, LIFT, o);
+    return;
+  }
   for (size_t i = 0; i < OPB; ++i) o[i] = 0;
   if constexpr (USE_MMA) {  // A fragments: lane -> (row 8g + lane/4, column 4k + lane%4)
     T* av = reinterpret_cast<T*>(o);
@@ -1343,15 +1361,15 @@ dg::KernelInfo info() {
   dg::KernelInfo k;
   k.N = N;
   k.prec = (int)sizeof(T);
-  k.threads = TEAM;
-  k.slots = nslots(true, false);
+  k.threads = USE_TC ? tc::NTH : TEAM;
+  k.slots = USE_TC ? 1 : nslots(true, false);
   k.row_groups = P;
   k.rows_per_group = R;
-  k.smem_bytes = smem_total(nslots(true, false), true, false, true);
-  k.contraction = USE_TF ? 2 : (USE_MMA ? 1 : 0);
+  k.smem_bytes = USE_TC ? tc::smem_bytes(false) : smem_total(nslots(true, false), true, false, true);
+  k.contraction = USE_TC ? 3 : (USE_TF ? 2 : (USE_MMA ? 1 : 0));
   k.residual_tma = RES_TMA ? 1 : 0;
   k.teams_cap = DG_C;
-  k.flags = (FLUX_FIRST ? 1 : 0) | (OPS_GLOBAL ? 2 : 0) | (FX ? 4 : 0) | (USE_TF && IL ? 8 : 0);
+  k.flags = USE_TC ? 0 : (FLUX_FIRST ? 1 : 0) | (OPS_GLOBAL ? 2 : 0) | (FX ? 4 : 0) | (USE_TF && IL ? 8 : 0);
   return k;
 }
 
@@ -1368,6 +1386,8 @@ KernelModule DG_CAT(dg_module_, DG_TAG)() {
   m.info = &info;
   m.check_fmask = &check_fmask;
   m.swizzle = SWM;
+  m.tile_group = USE_TC ? tc::TG : 1;
+  m.variant = DG_VARIANT;
   return m;
 }
 }  // namespace dg

@@ -29,14 +29,14 @@ namespace dg {
 #include "modules.inc"
 #undef DG_MODULE
 
-const KernelModule* find_module(int N, int prec) {
+const KernelModule* find_module(int N, int prec, int variant) {
   static const std::vector<KernelModule> mods = {
 #define DG_MODULE(tag) dg_module_##tag(),
 #include "modules.inc"
 #undef DG_MODULE
   };
   for (const auto& m : mods)
-    if (m.N == N && m.prec == prec) return &m;
+    if (m.N == N && m.prec == prec && m.variant == variant) return &m;
   return nullptr;
 }
 }  // namespace dg
@@ -181,7 +181,7 @@ int grid_for(int64_t n) {
 struct dg_ctx {
   // options
   int N = 0, prec = 8, device = -1, rank = 0, nranks = 1, fused = 1, transport = 0;
-  int max_ctas = 0, tile_order = 0, check_every = 0;
+  int max_ctas = 0, tile_order = 0, check_every = 0, kernel_variant = 0;
   double alpha = 1.0;
   bool host_only = true, poisoned = false, material = false;
   // host setup
@@ -191,6 +191,7 @@ struct dg_ctx {
   const dg::KernelModule* km = nullptr;
   // sizes
   int64_t Kl = 0, ntiles = 0, Kpad = 0, fstride = 0, vstride = 0, n_send = 0, n_recv = 0, ghost_base = 0;
+  int64_t group = 1, ngroups = 0;  // tiles per kernel work unit (KernelModule::tile_group), units
   size_t tsz = 8;
   int ngeo = dg::NGEO_CONST;
   // device buffers
@@ -310,7 +311,7 @@ dg::StageArgs base_args(dg_ctx* c) {
   a.tiles = nullptr;
   a.fstride = c->fstride;
   a.vstride = c->vstride;
-  a.ntiles = (int32_t)c->ntiles;
+  a.ntiles = (int32_t)c->ngroups;
   a.write_res = 1;
   a.scale_volume = 0;
   a.alpha = c->alpha;
@@ -436,10 +437,12 @@ void upload_geometry(dg_ctx* c, std::vector<T>& g, std::vector<int32_t>& vp, con
   // blocked (column-swizzled) offset of node n of the element in device slot d
   auto col = [&](int64_t d, int n) -> int64_t { return dg::swz_col(swm, n, (int)(d & 31)); };
   auto blk = [&](int64_t d, int n) -> int64_t { return ((d >> 5) * Np + n) * 32 + col(d, n); };
-  // neighbour node n of the element in slot d2, seen from slot d: same tile -> shared-memory
-  // offset within the tile's field block, encoded negative: -(1 + n*32 + column)
+  // neighbour node n of the element in slot d2, seen from slot d: same work unit (group of
+  // c->group tiles) -> shared-memory offset within the unit's field block, encoded negative:
+  // -(1 + (tile-in-group * Np + n) * 32 + column)
+  const int64_t gsz = 32 * c->group;
   auto nbr_code = [&](int64_t d, int64_t d2, int n) -> int64_t {
-    if ((d >> 5) == (d2 >> 5)) return -(1 + (int64_t)n * 32 + col(d2, n));
+    if (d / gsz == d2 / gsz) return -(1 + (((d2 >> 5) % c->group) * Np + n) * 32 + col(d2, n));
     return blk(d2, n);
   };
   for (int64_t d = 0; d < c->Kpad; ++d) {
@@ -509,10 +512,11 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
     return set_err(DG_E_CUDA, std::string("no usable CUDA device: ") + cudaGetErrorString(e));
   if (c->device >= ndev) return set_err(DG_E_ARG, "device ordinal out of range");
   CU(c, cudaSetDevice(c->device));
-  c->km = dg::find_module(c->N, c->prec);
+  c->km = dg::find_module(c->N, c->prec, c->kernel_variant);
   if (!c->km)
     return set_err(DG_E_DEGREE, "no kernel module compiled for N=" + std::to_string(c->N) +
-                                    " precision=" + std::to_string(c->prec));
+                                    " precision=" + std::to_string(c->prec) +
+                                    " variant=" + std::to_string(c->kernel_variant));
   if (!c->km->check_fmask(c->ref.Fmask.data()))
     return set_err(DG_E_STATE, "kernel face masks disagree with the setup's node set");
   {
@@ -526,7 +530,9 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
   c->tsz = (size_t)c->prec;
   c->ngeo = c->material ? dg::NGEO_MAT : dg::NGEO_CONST;
   c->Kl = (int64_t)c->mesh.local.size();
-  c->ntiles = (c->Kl + 31) / 32;
+  c->group = c->km->tile_group;
+  c->ngroups = (c->Kl + 32 * c->group - 1) / (32 * c->group);
+  c->ntiles = c->ngroups * c->group;
   c->Kpad = c->ntiles * 32;
   c->n_recv = (int64_t)c->mesh.recv_gdof.size();
   c->n_send = (int64_t)c->mesh.send_gdof.size();
@@ -591,10 +597,12 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
     if ((st = alloc(c, &c->sendbuf, 3 * c->n_send * c->tsz)) != DG_OK) return st;
   }
   {
-    std::vector<char> bnd(c->ntiles, 0);
-    for (int64_t p = 0; p < c->n_recv; ++p) bnd[c->slot_of[c->mesh.recv_point[p] / (3 * c->ref.Nfp)] >> 5] = 1;
+    // interior / partition-boundary classes of the kernels' work units (groups of tiles)
+    std::vector<char> bnd(c->ngroups, 0);
+    for (int64_t p = 0; p < c->n_recv; ++p)
+      bnd[(c->slot_of[c->mesh.recv_point[p] / (3 * c->ref.Nfp)] >> 5) / c->group] = 1;
     std::vector<int32_t> ti, tb;
-    for (int64_t t = 0; t < c->ntiles; ++t) (bnd[t] ? tb : ti).push_back((int32_t)t);
+    for (int64_t t = 0; t < c->ngroups; ++t) (bnd[t] ? tb : ti).push_back((int32_t)t);
     c->n_int = (int32_t)ti.size();
     c->n_bnd = (int32_t)tb.size();
     if ((st = alloc(c, (void**)&c->tiles_int, std::max<size_t>(ti.size(), 1) * sizeof(int32_t))) != DG_OK) return st;
@@ -665,6 +673,7 @@ dg_status dg_options_default(dg_options* o) {
   o->max_ctas = 0;
   o->tile_order = 0;
   o->check_every = 0;
+  o->kernel_variant = 0;
   return DG_OK;
 }
 
@@ -680,6 +689,9 @@ dg_status dg_setup(const dg_options* o, int64_t Nv, const double* VX, const doub
   if (!(o->alpha >= 0.0)) return set_err(DG_E_ARG, "alpha must be >= 0");
   if (o->max_ctas < 0 || o->check_every < 0 || (o->tile_order != 0 && o->tile_order != 1))
     return set_err(DG_E_ARG, "max_ctas and check_every must be >= 0, tile_order 0 or 1");
+  if (o->kernel_variant != 0 && o->kernel_variant != 1) return set_err(DG_E_ARG, "kernel_variant must be 0 or 1");
+  if (o->kernel_variant == 1 && o->precision != 4)
+    return set_err(DG_E_ARG, "kernel_variant 1 (tcgen05) is an fp32 path");
   if (eps)
     for (int64_t k = 0; k < K; ++k)
       if (!(eps[k] > 0.0) || !(mu[k] > 0.0)) return set_err(DG_E_ARG, "eps and mu must be > 0");
@@ -695,6 +707,7 @@ dg_status dg_setup(const dg_options* o, int64_t Nv, const double* VX, const doub
   c->max_ctas = o->max_ctas;
   c->tile_order = o->tile_order;
   c->check_every = o->check_every;
+  c->kernel_variant = o->kernel_variant;
   c->material = eps != nullptr;
   try {
     c->ref = dg::build_refelem(o->N);
@@ -1178,7 +1191,7 @@ dg_status dg_get_kernel_config(const dg_ctx* c, dg_kernel_config* out) {
   dg_status st = check_usable(c, false);
   if (st != DG_OK) return st;
   if (!out) return set_err(DG_E_ARG, "null output");
-  const dg::KernelModule* km = c->km ? c->km : dg::find_module(c->N, c->prec);  // host-only: lookup
+  const dg::KernelModule* km = c->km ? c->km : dg::find_module(c->N, c->prec, c->kernel_variant);  // host-only
   if (!km) return set_err(DG_E_DEGREE, "no kernel module compiled for N=" + std::to_string(c->N));
   const dg::KernelInfo k = km->info();
   out->contraction = k.contraction;

@@ -48,7 +48,8 @@ class Options(C.Structure):
                 ("device", C.c_int32), ("alpha", C.c_double), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("fused", C.c_int32), ("transport", C.c_int32),
                 ("nccl_id", C.c_void_p), ("part", C.c_void_p), ("stream", C.c_void_p),
-                ("max_ctas", C.c_int32), ("tile_order", C.c_int32), ("check_every", C.c_int32)]
+                ("max_ctas", C.c_int32), ("tile_order", C.c_int32), ("check_every", C.c_int32),
+                ("kernel_variant", C.c_int32)]
 
 
 class KernelStats(C.Structure):
@@ -64,7 +65,7 @@ class KernelConfig(C.Structure):
                 ("smem_bytes", C.c_int64)]
 
 
-CONTRACTION = ("fma", "dmma_fp64", "3xtf32")
+CONTRACTION = ("fma", "dmma_fp64", "3xtf32", "tcgen05_3xtf32")
 
 _vp = C.c_void_p
 _i64 = C.c_int64
@@ -312,7 +313,7 @@ class Context:
 
 def dg_setup(N, VX, VY, EToV, eps=None, mu=None, bctag=None, precision=8, device=0, alpha=1.0,
              rank=0, nranks=1, fused=True, transport=0, nccl_id=None, part=None, stream=None,
-             max_ctas=0, tile_order=0, check_every=0):
+             max_ctas=0, tile_order=0, check_every=0, kernel_variant=0):
     """dg_setup: build a context for ``rank`` of ``nranks`` on the GLOBAL mesh (VX, VY, EToV)."""
     VX = _as(VX, np.float64)
     VY = _as(VY, np.float64)
@@ -334,6 +335,7 @@ def dg_setup(N, VX, VY, EToV, eps=None, mu=None, bctag=None, precision=8, device
     o.part = _ptr(part_a)
     o.stream = stream
     o.max_ctas, o.tile_order, o.check_every = int(max_ctas), int(tile_order), int(check_every)
+    o.kernel_variant = {"tuned": 0, "tcgen05": 1}.get(kernel_variant, kernel_variant)
     h = C.c_void_p()
     _check(_lib.dg_setup(C.byref(o), VX.size, _ptr(VX), _ptr(VY), K, _ptr(EToV), _ptr(eps_a), _ptr(mu_a),
                          _ptr(bc_a), C.byref(h)))

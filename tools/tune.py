@@ -114,7 +114,7 @@ for N in range(1, 10):
         # oracle gate: 100 steps on the stored case, grid capped (multi-tile pipeline), per-field A14
         g = c = dg.dg_setup(N, G["VX"], G["VY"], G["EToV"], precision=prec, max_ctas=2)
         xg, yg = g.nodes()
-        q0 = dginputs.cavity_mode(xg, yg, float(G["t0"]))
+        q0 = dginputs.cavity_mode(xg, yg, float(G["t0_%d" % N]))
         q0 = tuple(a + b for a, b in zip(q0, dginputs.perturbation(xg.shape, float(G["amplitude"]), seed=N)))
         g.set_fields(*q0); g.run(float(G["dt%d" % N]), int(G["steps"])); got = g.get_fields(); g.destroy()
         gate = max(float(np.abs(a - G[nm + str(N)]).max() / np.abs(G[nm + str(N)]).max())
