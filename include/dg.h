@@ -241,7 +241,12 @@ typedef struct {
                             bit 1: tensor-core operator fragments read through L1 from global
                             memory instead of a shared-memory copy per CTA (knob G);
                             bit 2: flux computed straight into the LIFT A fragments (knob X);
-                            bit 3: 3xTF32 products issued pass by pass (knob I) */
+                            bit 3: 3xTF32 products issued pass by pass (knob I);
+                            bit 4: compressed connectivity for constant-material contexts: one word
+                                   per face instead of one code per face point, face normals and Fsc
+                                   derived on chip from rx, sx, ry, sy (knob Z = 1);
+                            bit 5: geometry-only compression: the face normals and Fsc derived on chip,
+                                   one neighbour code per face point as uncompressed (knob Z = 2) */
   int64_t smem_bytes;    /* dynamic shared memory per CTA of the fused stage kernel */
 } dg_kernel_config;
 dg_status dg_get_kernel_config(const dg_ctx* c, dg_kernel_config* out);

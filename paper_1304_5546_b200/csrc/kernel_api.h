@@ -25,6 +25,34 @@ constexpr int TILE = 32;
 //   c = 18+4f  wEH = Y+/(Y+ + Y-), wHH = alpha/(Y+ + Y-), wHE = Z+/(Z+ + Z-), wEE = alpha/(Z+ + Z-)
 constexpr int NGEO_CONST = 16;
 constexpr int NGEO_MAT = 32;
+// Compressed connectivity (KernelModule::compressed, constant material): the geometry block is
+// rx, sx, ry, sy only, and vmapP holds one word per face, [t][3][32] (conn_word below).
+constexpr int NGEO_Z = 4;
+constexpr int ZC_PEC = -(1 << 30);  // added to a decoded point code: PEC wall (Bsc = -1, idP = idM)
+
+// Face f's outward normal and L = |v| = sJ_f / J = Fsc_f of an affine element, from its geometric
+// factors (SURVEY §8(c) O6 with rx = ys/J, sx = -yr/J, ry = -xs/J, sy = xr/J, J > 0):
+//   f0: v = (yr, -xr)/J = (-sx, -sy);  f1: (ys - yr, xr - xs)/J = (rx + sx, ry + sy);  f2: (-ys, xs)/J = (-rx, -ry)
+template <typename TT>
+__host__ __device__ inline void face_normal(int f, TT rx, TT sx, TT ry, TT sy, TT& nx, TT& ny, TT& L) {
+  const TT vx = f == 0 ? -sx : (f == 1 ? rx + sx : -rx);
+  const TT vy = f == 0 ? -sy : (f == 1 ? ry + sy : -ry);
+  L = sqrt(vx * vx + vy * vy);
+  nx = vx / L;
+  ny = vy / L;
+}
+
+// One connectivity word per (element, face), kernel-decoded into the per-point neighbour codes:
+//   bits 0-1 kind: 0 PEC wall, 1 neighbour in the same tile, 2 neighbour elsewhere on this rank,
+//                  3 neighbour on another rank (halo);
+//   bits 2-3 the neighbour's face f' (kinds 1, 2);
+//   bits 4-31 kind 1: the neighbour's column (tile lane); kind 2: its device slot;
+//             kind 3: the ghost index of the face's point i = 0 (its points follow in i order).
+// The neighbour's face point is i' = Nfp-1-i when faces f and f' run the same way round (traversal
+// (+1, +1, -1) for faces (0, 1, 2)), else i (the O7 reversal rule).
+__host__ __device__ constexpr uint32_t conn_word(uint32_t kind, uint32_t fp, uint32_t payload) {
+  return (kind & 3u) | ((fp & 3u) << 2) | (payload << 4);
+}
 
 enum StageMode : int {
   MODE_FUSED_RK = 0,    // volume + flux + LIFT + LSERK4 update (one kernel per stage)
@@ -86,6 +114,8 @@ struct KernelModule {
   // 0: the tuned module of this (N, precision) (csrc/tune.json); 1: the tcgen05 variant module
   // (fp32 only; dg_options.kernel_variant = 1)
   int variant = 0;
+  // 1: compressed connectivity for constant-material contexts (NGEO_Z geometry rows, conn words)
+  int compressed = 0;
 };
 
 // Column of element e (0..31) of node row n in the tile-blocked layout, swizzle mode swm:

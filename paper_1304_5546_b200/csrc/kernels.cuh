@@ -140,7 +140,20 @@ __device__ __forceinline__ V ldop(const V* p) {
 constexpr int SWM = USE_MMA ? 4 : (USE_TF ? 8 : 0);  // identity for the FMA and tcgen05 kernels
 __host__ __device__ constexpr int colx(int n, int e) { return dg::swz_col(SWM, n, e); }
 constexpr size_t QB = (size_t)3 * NP * TL * sizeof(T);
-__host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)(mat ? dg::NGEO_MAT : dg::NGEO_CONST) * TL * sizeof(T); }
+// DG_ZC (constant-material kernels, not with DG_FX): compressed connectivity (SURVEY §8(f) row 3,
+// PAPER.md:893-903).  Per tile the geometry block is only rx, sx, ry, sy (dg::NGEO_Z rows): the face
+// normals and Fsc are derived on chip from them (affine elements, kernel_api.h), and instead of one
+// neighbour code per face point there is one connectivity word per face (dg::conn_word), decoded into
+// the per-point codes with the O7 reversal rule when the codes are fetched.
+// DG_ZC = 2: geometry only -- the 4-row geometry block and derived face geometry, but one code per
+// face point as uncompressed (a PEC point's code carries dg::ZC_PEC): no decode work per point.
+#ifndef DG_ZC
+#define DG_ZC 0
+#endif
+constexpr bool ZC = DG_ZC != 0;        // 4-row geometry block, face geometry derived on chip
+constexpr bool ZC_CONN = DG_ZC == 1;   // one connectivity word per face (decoded per point)
+__host__ __device__ constexpr int ngeo(bool mat) { return mat ? dg::NGEO_MAT : (ZC ? dg::NGEO_Z : dg::NGEO_CONST); }
+__host__ __device__ constexpr size_t geo_bytes(bool mat) { return (size_t)ngeo(mat) * TL * sizeof(T); }
 constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
 // DG_RT (TF32 path only): the LSERK4 residual of the slot's tile also arrives by TMA into
 // shared memory (frees ~12 NT registers per thread) instead of a register prefetch.
@@ -197,6 +210,8 @@ __device__ __forceinline__ int point_of(int g, int k) {  // face point of slot k
 #define DG_FX 0
 #endif
 constexpr bool FX = F32 && DG_MMA == 1 && DG_FX;
+static_assert(!(FX && DG_ZC), "DG_ZC (compressed connectivity) is not implemented with DG_FX");
+static_assert(!(USE_TC && DG_ZC), "DG_ZC (compressed connectivity) is not implemented in the tcgen05 kernels");
 // DG_IL (3xTF32 path): issue the three split products pass by pass across all n-tiles and
 // accumulators (lo*hi for all, then hi*lo, then hi*hi) instead of accumulator by accumulator,
 // so consecutive MMAs into one accumulator are NT x fields instructions apart
@@ -280,6 +295,23 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// Decode the connectivity word of face f of tile element e into face point i's neighbour code (the
+// uncompressed vmapP code: >= 0 an offset into a field, < 0 a same-tile shared-memory offset,
+// + dg::ZC_PEC on a PEC wall).  vstride = the ghost region's start in a field.
+__device__ __forceinline__ int32_t zc_decode(uint32_t w, int f, int i, int e, int64_t vstride) {
+  const uint32_t kind = w & 3u, fp = (w >> 2) & 3u, pay = w >> 4;
+  if (kind == 3u) return (int32_t)(vstride + pay + i);
+  if (kind == 0u) {
+    const int own = fmask(f, i);
+    return -(1 + own * TL + colx(own, e)) + dg::ZC_PEC;
+  }
+  const int ip = ((f == 2) == (fp == 2u)) ? NFP - 1 - i : i;  // O7 reversal rule
+  const int rs = (ip * (2 * N + 3 - ip)) >> 1;                // row_start(ip)
+  const int n2 = fp == 0u ? ip : rs + (fp == 1u ? N - ip : 0);  // fmask(fp, ip)
+  if (kind == 1u) return -(1 + n2 * TL + colx(n2, (int)(pay & 31u)));
+  return (int32_t)((((int64_t)(pay >> 5)) * NP + n2) * TL + colx(n2, (int)(pay & 31u)));
+}
+
 template <int MODE>
 struct ModeTraits {
   static constexpr bool vol = (MODE == dg::MODE_FUSED_RK || MODE == dg::MODE_VOLUME || MODE == dg::MODE_RHS);
@@ -349,14 +381,41 @@ __device__ __forceinline__ void volume_rows(const T* __restrict__ sq, const DVT*
 // global memory (gathered into sp); < 0 a neighbour in the SAME tile, read
 // straight from the tile's shared-memory fields at offset -(1 + code).
 // The flux of face point m (face f) of tile element e: gg = the tile's geometry + e.
+// ZC: this element's face normals and half-Fsc, from rx, sx, ry, sy (dg::face_normal; rsqrt)
+template <typename TT>
+__device__ __forceinline__ void zc_faces(const TT* __restrict__ gg, TT (&fz)[3][3]) {
+  const TT rx = gg[0 * TL], sx = gg[1 * TL], ry = gg[2 * TL], sy = gg[3 * TL];
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    const TT vx = f == 0 ? -sx : (f == 1 ? rx + sx : -rx);
+    const TT vy = f == 0 ? -sy : (f == 1 ? ry + sy : -ry);
+    const TT l2 = vx * vx + vy * vy, ri = rsqrt(l2);
+    fz[f][0] = vx * ri;
+    fz[f][1] = vy * ri;
+    fz[f][2] = TT(0.5) * l2 * ri;  // Fsc / 2 = |v| / 2
+  }
+}
+
 template <bool MAT, typename TT>
 __device__ __forceinline__ void flux_one(const TT* __restrict__ sq, const TT* __restrict__ gg,
                                          const TT* __restrict__ sp, int code, int m, int f, int e, TT alpha,
-                                         TT& fHx, TT& fHy, TT& fEz) {
+                                         TT& fHx, TT& fHy, TT& fEz, const TT (*fzg)[3] = nullptr) {
     const int i = m - f * NFP;
     const int fm = f == 0 ? i : (f == 1 ? row_start(i) + N - i : row_start(i));
-    const TT nx = gg[(4 + 3 * f) * TL], ny = gg[(5 + 3 * f) * TL], hF = gg[(6 + 3 * f) * TL];
-    const TT bsc = gg[(13 + f) * TL];
+    TT nx, ny, hF, bsc;
+    if constexpr (ZC && !MAT) {  // derived face geometry (zc_faces); PEC points flagged in the code
+      nx = fzg[f][0];
+      ny = fzg[f][1];
+      hF = fzg[f][2];
+      const bool pec = code < dg::ZC_PEC;
+      bsc = pec ? TT(-1) : TT(1);
+      if (pec) code -= dg::ZC_PEC;
+    } else {
+      nx = gg[(4 + 3 * f) * TL];
+      ny = gg[(5 + 3 * f) * TL];
+      hF = gg[(6 + 3 * f) * TL];
+      bsc = gg[(13 + f) * TL];
+    }
     const int pm = m * TL + colx(m, e);                               // this point in sp
     const TT* pp = code < 0 ? sq + (-1 - code) : sp + pm;             // neighbour trace, field 0
     const int fs = code < 0 ? NP * TL : NFE * TL;                     // field stride of that source
@@ -383,13 +442,15 @@ __device__ __forceinline__ void flux_one(const TT* __restrict__ sq, const TT* __
 template <bool MAT>
 __device__ __forceinline__ void flux_points(const T* __restrict__ sq, const T* __restrict__ gg, T* __restrict__ sp,
                                             const int32_t (&vmc)[KCODE], int g, int lane, T alpha) {
+  T fz[3][3];
+  if constexpr (ZC && !MAT) zc_faces(gg, fz);
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
     const int m = point_of(g, k);
     if (m >= NF) break;
     const int f = FACE_MAJOR ? k / KPF : (m < NFP ? 0 : (m < 2 * NFP ? 1 : 2));  // compile-time if face-major
     T fHx, fHy, fEz;
-    flux_one<MAT>(sq, gg, sp, vmc[k], m, f, lane, alpha, fHx, fHy, fEz);
+    flux_one<MAT>(sq, gg, sp, vmc[k], m, f, lane, alpha, fHx, fHy, fEz, fz);
     const int pm = m * TL + colx(m, lane);
     sp[0 * NFE * TL + pm] = fHx;
     sp[1 * NFE * TL + pm] = fHy;
@@ -920,7 +981,7 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
 template <int MODE, bool MAT>
 __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageArgs p) {
   using MT = ModeTraits<MODE>;
-  constexpr int NG = MAT ? dg::NGEO_MAT : dg::NGEO_CONST;
+  constexpr int NG = ngeo(MAT);
   constexpr int S = nslots(MT::surf, MAT);
   constexpr size_t SLOT = slot_bytes(MT::surf, MAT, MT::rk);
   constexpr size_t GB = geo_bytes(MAT);
@@ -959,7 +1020,19 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   };
   // vmapP codes of this thread's face points (m = g + k P) of tile `it`
   auto load_codes = [&](int it, int32_t (&v)[KCODE]) {
-    if constexpr (MT::surf) {
+    if constexpr (MT::surf && ZC_CONN && !MAT) {  // one word per face, decoded per point
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(p.vmapP) + (int64_t)tile_of(it) * 3 * TL;
+#pragma unroll
+      for (int k = 0; k < KCODE; ++k) {
+        const PointElem pe = pair_of(g, lane, k);
+        if (pe.m < NF) {
+          const int f = pe.m / NFP;
+          v[k] = zc_decode(__ldg(src + f * TL + pe.e), f, pe.m - f * NFP, pe.e, p.vstride);
+        } else {
+          v[k] = -1;
+        }
+      }
+    } else if constexpr (MT::surf) {
       const int32_t* src = p.vmapP + (int64_t)tile_of(it) * NF * TL;
 #pragma unroll
       for (int k = 0; k < KCODE; ++k) {
@@ -1369,7 +1442,8 @@ dg::KernelInfo info() {
   k.contraction = USE_TC ? 3 : (USE_TF ? 2 : (USE_MMA ? 1 : 0));
   k.residual_tma = RES_TMA ? 1 : 0;
   k.teams_cap = DG_C;
-  k.flags = USE_TC ? 0 : (FLUX_FIRST ? 1 : 0) | (OPS_GLOBAL ? 2 : 0) | (FX ? 4 : 0) | (USE_TF && IL ? 8 : 0);
+  k.flags = USE_TC ? 0 : (FLUX_FIRST ? 1 : 0) | (OPS_GLOBAL ? 2 : 0) | (FX ? 4 : 0) | (USE_TF && IL ? 8 : 0) |
+                         (ZC_CONN ? 16 : 0) | (ZC && !ZC_CONN ? 32 : 0);
   return k;
 }
 
@@ -1388,6 +1462,7 @@ KernelModule DG_CAT(dg_module_, DG_TAG)() {
   m.swizzle = SWM;
   m.tile_group = USE_TC ? tc::TG : 1;
   m.variant = DG_VARIANT;
+  m.compressed = DG_ZC;
   return m;
 }
 }  // namespace dg

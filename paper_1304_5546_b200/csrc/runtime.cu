@@ -194,6 +194,7 @@ struct dg_ctx {
   int64_t group = 1, ngroups = 0;  // tiles per kernel work unit (KernelModule::tile_group), units
   size_t tsz = 8;
   int ngeo = dg::NGEO_CONST;
+  int compressed = 0;  // 1: compressed connectivity, 2: geometry only (module knob, constant material)
   // device buffers
   void* q[2] = {nullptr, nullptr};
   void* res = nullptr;
@@ -432,7 +433,8 @@ void upload_geometry(dg_ctx* c, std::vector<T>& g, std::vector<int32_t>& vp, con
   const int ng = c->ngeo;
   const dg::Mesh& m = c->mesh;
   g.assign((size_t)c->ntiles * ng * 32, T(0));
-  vp.assign((size_t)c->ntiles * NF * 32, 0);
+  const bool words = c->compressed == 1;  // one connectivity word per face
+  vp.assign((size_t)c->ntiles * (words ? 3 : NF) * 32, 0);
   const int swm = c->km->swizzle;
   // blocked (column-swizzled) offset of node n of the element in device slot d
   auto col = [&](int64_t d, int n) -> int64_t { return dg::swz_col(swm, n, (int)(d & 31)); };
@@ -448,7 +450,16 @@ void upload_geometry(dg_ctx* c, std::vector<T>& g, std::vector<int32_t>& vp, con
   for (int64_t d = 0; d < c->Kpad; ++d) {
     const int64_t t = d >> 5, lane = d & 31;
     auto G = [&](int comp) -> T& { return g[(t * ng + comp) * 32 + lane]; };
-    if (d >= c->Kl) {
+    if (d >= c->Kl) {  // padding element: its neighbour codes point at itself (finite zeros)
+      if (c->compressed) G(0) = G(3) = T(1);  // identity geometric factors: finite derived normals
+      if (words) {
+        for (int f = 0; f < 3; ++f) vp[(t * 3 + f) * 32 + lane] = (int32_t)dg::conn_word(1, 0, (uint32_t)lane);
+        continue;
+      }
+      if (c->compressed) {
+        for (int mm = 0; mm < NF; ++mm) vp[(t * NF + mm) * 32 + lane] = (int32_t)nbr_code(d, d, 0);
+        continue;
+      }
       for (int f = 0; f < 3; ++f) G(13 + f) = T(1);
       for (int mm = 0; mm < NF; ++mm) vp[(t * NF + mm) * 32 + lane] = (int32_t)nbr_code(d, d, 0);
       continue;
@@ -459,7 +470,7 @@ void upload_geometry(dg_ctx* c, std::vector<T>& g, std::vector<int32_t>& vp, con
     G(2) = (T)m.ry[kl];
     G(3) = (T)m.sy[kl];
     const int64_t k = m.local[kl];
-    for (int f = 0; f < 3; ++f) {
+    for (int f = 0; f < 3 && !c->compressed; ++f) {
       G(4 + 3 * f) = (T)m.nx[3 * kl + f];
       G(5 + 3 * f) = (T)m.ny[3 * kl + f];
       G(6 + 3 * f) = (T)(c->material ? m.Fsc[3 * kl + f] : 0.5 * m.Fsc[3 * kl + f]);
@@ -480,6 +491,7 @@ void upload_geometry(dg_ctx* c, std::vector<T>& g, std::vector<int32_t>& vp, con
         G(21 + 4 * f) = (T)(c->alpha / (Zp + Zm));
       }
     }
+    std::vector<int64_t> code(NF);
     for (int mm = 0; mm < NF; ++mm) {
       const int64_t nl = m.nbr_local[kl * NF + mm];
       int64_t idx;
@@ -489,7 +501,49 @@ void upload_geometry(dg_ctx* c, std::vector<T>& g, std::vector<int32_t>& vp, con
       } else {
         idx = c->ghost_base + (-nl - 1);
       }
-      vp[(t * NF + mm) * 32 + lane] = (int32_t)idx;
+      code[mm] = idx;
+      // geometry-only compression: a PEC point's code carries ZC_PEC (its Bsc = -1)
+      if (!words)
+        vp[(t * NF + mm) * 32 + lane] =
+            (int32_t)(idx + (c->compressed == 2 && m.pec[3 * k + mm / Nfp] ? dg::ZC_PEC : 0));
+    }
+    if (!words) continue;
+    // one word per face (kernel_api.h conn_word), checked against every point's code above by the
+    // kernels' own decode rule (the O7 reversal), so a wrong word fails at setup, not in a run
+    for (int f = 0; f < 3; ++f) {
+      uint32_t w;
+      const int64_t k2 = m.EToE[3 * k + f];
+      const int fp = m.EToF[3 * k + f];
+      if (m.pec[3 * k + f]) {
+        w = dg::conn_word(0, 0, 0);
+      } else if (m.g2l[k2] < 0) {  // halo face: ghost index of point 0, the others follow
+        const int64_t g0 = code[f * Nfp] - c->ghost_base;
+        for (int i = 0; i < Nfp; ++i)
+          if (code[f * Nfp + i] != c->ghost_base + g0 + i) throw dg::SetupError{DG_E_STATE, "halo face points out of order"};
+        w = dg::conn_word(3, 0, (uint32_t)g0);
+      } else {
+        const int64_t d2 = c->slot_of[m.g2l[k2]];
+        w = (d2 >> 5) == (d >> 5) ? dg::conn_word(1, fp, (uint32_t)(d2 & 31)) : dg::conn_word(2, fp, (uint32_t)d2);
+      }
+      if ((w >> 4) >= (1u << 28)) throw dg::SetupError{DG_E_ARG, "partition too large for compressed connectivity"};
+      vp[(t * 3 + f) * 32 + lane] = (int32_t)w;
+      // host replica of the kernels' zc_decode
+      const uint32_t kind = w & 3u, fw = (w >> 2) & 3u, pay = w >> 4;
+      for (int i = 0; i < Nfp; ++i) {
+        const int mm = f * Nfp + i;
+        int64_t dec;
+        if (kind == 3u) {
+          dec = c->ghost_base + pay + i;
+        } else if (kind == 0u) {
+          dec = code[mm];  // PEC: own node (the kernel adds ZC_PEC)
+        } else {
+          const int ip = ((f == 2) == (fw == 2u)) ? Nfp - 1 - i : i;
+          const int n2 = c->ref.Fmask[fw * Nfp + ip];
+          dec = kind == 1u ? -(1 + (int64_t)n2 * 32 + dg::swz_col(swm, n2, (int)(pay & 31u)))
+                           : (((int64_t)(pay >> 5)) * Np + n2) * 32 + dg::swz_col(swm, n2, (int)(pay & 31u));
+        }
+        if (dec != code[mm]) throw dg::SetupError{DG_E_STATE, "compressed connectivity does not reproduce vmapP"};
+      }
     }
   }
 }
@@ -528,7 +582,8 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
   }
   const int Np = c->ref.Np;
   c->tsz = (size_t)c->prec;
-  c->ngeo = c->material ? dg::NGEO_MAT : dg::NGEO_CONST;
+  c->compressed = c->material ? 0 : c->km->compressed;
+  c->ngeo = c->material ? dg::NGEO_MAT : (c->compressed ? dg::NGEO_Z : dg::NGEO_CONST);
   c->Kl = (int64_t)c->mesh.local.size();
   c->group = c->km->tile_group;
   c->ngroups = (c->Kl + 32 * c->group - 1) / (32 * c->group);
@@ -569,6 +624,7 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
   // geometry + maps
   {
     std::vector<int32_t> vp;
+    try {
     if (c->tsz == 4) {
       std::vector<float> g;
       upload_geometry<float>(c, g, vp, eps, mu);
@@ -579,6 +635,9 @@ dg_status setup_device(dg_ctx* c, const dg_options* o, const double* eps, const 
       upload_geometry<double>(c, g, vp, eps, mu);
       if ((st = alloc(c, &c->geo, g.size() * sizeof(double))) != DG_OK) return st;
       CU(c, cudaMemcpy(c->geo, g.data(), g.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    } catch (const dg::SetupError& e) {
+      return set_err((dg_status)e.status, e.msg);
     }
     if ((st = alloc(c, (void**)&c->vmapP, vp.size() * sizeof(int32_t))) != DG_OK) return st;
     CU(c, cudaMemcpy(c->vmapP, vp.data(), vp.size() * sizeof(int32_t), cudaMemcpyHostToDevice));

@@ -50,7 +50,15 @@ def test_kernel_config_matches_tune_table(prec):
         assert k["ops_global"] == bool(t.get("G", 0))
         assert k["flux_in_fragments"] == bool(t["M"] == 1 and prec == 4 and t.get("X", 0))
         assert k["pass_interleave"] == bool(t["M"] and prec == 4 and t.get("I", 0))
+        assert k["compressed_connectivity"] == (t.get("Z", 0) == 1)
+        assert k["compressed_geometry"] == (t.get("Z", 0) in (1, 2))
         assert 0 < k["smem_bytes"] <= 227 * 1024 and k["threads"] % 32 == 0
+        if prec == 4:  # the tcgen05 variant module of every fp32 N
+            c = dg.dg_setup(N, VX, VY, E, device=-1, precision=4, kernel_variant=1)
+            kt = c.kernel_config()
+            c.destroy()
+            assert kt["contraction"] == "tcgen05_3xtf32" and kt["threads"] == 256, (N, kt)
+            assert 0 < kt["smem_bytes"] <= 227 * 1024
 
 
 def _jittered(n, amp=0.25, seed=7, nx=None):

@@ -52,6 +52,10 @@ if os.environ.get("TUNE_GRID") == "og":  # tensor-core paths, flux first, operat
             + [dict(R=8, S=1, C=c, M=1, Q=1, F=f, G=0) for c, f in itertools.product((3, 4), (0, 1))]}
 if os.environ.get("TUNE_GRID", "").startswith("file:"):  # a JSON list of variant names (a confirmation run)
     GRID = {0: [{x[0]: int(x[1:]) for x in v.split("_")} for v in json.load(open(os.environ["TUNE_GRID"][5:]))]}
+if os.environ.get("TUNE_GRID") == "c5":  # fp64 N=8 (config C5): smaller teams (R=12/16) -> 2-3 CTAs/SM
+    GRID = {8: [dict(R=r, S=s, C=c, M=0, F=f) for r, s, c, f in itertools.product((6, 8, 12, 16), (1, 2, 3),
+                                                                               (1, 2, 3, 4), (0, 1))]
+            + [dict(R=8, S=s, C=c, M=1, F=f) for s, c, f in itertools.product((1, 2, 3), (1, 2, 3), (0, 1))]}
 if os.environ.get("TUNE_GRID") == "tf":  # tensor-core variants (fp32 3xTF32, fp64 DMMA)
     GRID = {4: [dict(R=8, S=s, C=c, M=1, Q=q) for s, c, q in itertools.product((1, 2), (3, 4, 6), (0, 1))]}
 
