@@ -181,3 +181,84 @@ def cfl_dt(VX, VY, EToV, N, cfl=1.0, eps=None, mu=None):
     g = np.sort(np.polynomial.legendre.leggauss(N + 1)[0])
     rmin = abs(g[1] - g[0]) if N >= 1 else 2.0
     return cfl * (2.0 / 3.0) * float(rin.min()) * rmin
+
+
+# ----------------------------------------------------------------------------
+# 3D (tetrahedral Maxwell, the paper's hedge workload)
+# ----------------------------------------------------------------------------
+def cube_tet_mesh(n: int):
+    """Structured tetrahedral mesh of [0,1]^3: n^3 cells, each split into the 6 Kuhn tetrahedra
+    (v000, v000 + e_a, v000 + e_a + e_b, v111) for the 6 axis orders (a, b, c) -- conforming across
+    cells.  Vertex id = i + (n+1)(j + (n+1)k).  Returns (VX, VY, VZ, EToV int64 [6 n^3][4]); the
+    elements come in either orientation (the setup re-orients them)."""
+    import itertools
+
+    if n < 1:
+        raise ValueError("n >= 1")
+    g = np.linspace(0.0, 1.0, n + 1)
+    K3 = np.arange(n + 1)
+    I, J, Kk = np.meshgrid(K3, K3, K3, indexing="ij")
+    vid = lambda i, j, k: i + (n + 1) * (j + (n + 1) * k)  # noqa: E731
+    VX = np.empty((n + 1) ** 3)
+    VY = np.empty_like(VX)
+    VZ = np.empty_like(VX)
+    VX[vid(I, J, Kk)] = g[I]
+    VY[vid(I, J, Kk)] = g[J]
+    VZ[vid(I, J, Kk)] = g[Kk]
+    ci, cj, ck = (a.ravel() for a in np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij"))
+    order = np.argsort(ck * n * n + cj * n + ci, kind="stable")  # cells x fastest
+    ci, cj, ck = ci[order], cj[order], ck[order]
+    tets = []
+    for perm in itertools.permutations(range(3)):
+        p = [np.zeros(3, dtype=np.int64)]
+        for ax in perm:
+            nxt = p[-1].copy()
+            nxt[ax] += 1
+            p.append(nxt)
+        tets.append(np.stack([vid(ci + q[0], cj + q[1], ck + q[2]) for q in p], axis=1))
+    EToV = np.stack(tets, axis=1).reshape(-1, 4)
+    return VX, VY, VZ, EToV
+
+
+# the (1,1,1) PEC cube-cavity mode, E = (a1 cos sin sin, a2 sin cos sin, a3 sin sin cos) cos(wt),
+# a1 + a2 + a3 = 0 (div E = 0), w = pi sqrt(3); H from dH/dt = -curl E
+CUBE_MODE_A = (1.0, -2.0, 1.0)
+
+
+def cube_cavity_mode(x, y, z, t, a=CUBE_MODE_A):
+    """Exact PEC unit-cube cavity mode (1,1,1) of mu dH/dt = -curl E, eps dE/dt = curl H (eps=mu=1).
+    Returns (Hx, Hy, Hz, Ex, Ey, Ez)."""
+    a1, a2, a3 = a
+    w = math.pi * math.sqrt(3.0)
+    sx, cx = np.sin(math.pi * x), np.cos(math.pi * x)
+    sy, cy = np.sin(math.pi * y), np.cos(math.pi * y)
+    sz, cz = np.sin(math.pi * z), np.cos(math.pi * z)
+    ct, st = math.cos(w * t), math.sin(w * t)
+    Ex = a1 * cx * sy * sz * ct
+    Ey = a2 * sx * cy * sz * ct
+    Ez = a3 * sx * sy * cz * ct
+    k = -(math.pi / w) * st  # H = -(curl E)(x) sin(wt) / w
+    Hx = k * (a3 - a2) * sx * cy * cz
+    Hy = k * (a1 - a3) * cx * sy * cz
+    Hz = k * (a2 - a1) * cx * cy * sz
+    return Hx, Hy, Hz, Ex, Ey, Ez
+
+
+def cube_balanced_start(T):
+    """Start time whose run of length T ends at phase w t = pi/4 (every field O(1))."""
+    w = math.pi * math.sqrt(3.0)
+    return math.pi / (4.0 * w) - T
+
+
+def cfl_dt_3d(VX, VY, VZ, EToV, N, cfl=1.0):
+    """dt = cfl * (2/3) * min_k r_in,k * (x1 - x0): inscribed radius of each tetrahedron (3 V / total
+    face area) times the first Gauss-Legendre node gap of order N+1 (the 2D estimate's rule)."""
+    P = np.stack([VX[EToV], VY[EToV], VZ[EToV]], axis=-1)
+    vol = np.abs(np.einsum("ki,ki->k", P[:, 1] - P[:, 0],
+                           np.cross(P[:, 2] - P[:, 0], P[:, 3] - P[:, 0]))) / 6.0
+    area = 0.0
+    for a, b, c in ((0, 1, 2), (0, 1, 3), (1, 2, 3), (0, 2, 3)):
+        area = area + 0.5 * np.linalg.norm(np.cross(P[:, b] - P[:, a], P[:, c] - P[:, a]), axis=1)
+    rin = 3.0 * vol / area
+    g, _ = np.polynomial.legendre.leggauss(N + 1)
+    return cfl * (2.0 / 3.0) * float(rin.min()) * float(g[1] - g[0])
