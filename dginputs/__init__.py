@@ -221,8 +221,10 @@ def cube_tet_mesh(n: int):
 
 
 # the (1,1,1) PEC cube-cavity mode, E = (a1 cos sin sin, a2 sin cos sin, a3 sin sin cos) cos(wt),
-# a1 + a2 + a3 = 0 (div E = 0), w = pi sqrt(3); H from dH/dt = -curl E
-CUBE_MODE_A = (1.0, -2.0, 1.0)
+# a1 + a2 + a3 = 0 (div E = 0), w = pi sqrt(3); H from dH/dt = -curl E has amplitudes
+# (a3 - a2, a1 - a3, a2 - a1) = (-5, 4, 1): all six components non-zero (a per-field check of a field
+# that is identically zero would only measure the perturbation)
+CUBE_MODE_A = (1.0, 2.0, -3.0)
 
 
 def cube_cavity_mode(x, y, z, t, a=CUBE_MODE_A):

@@ -1,0 +1,353 @@
+// Stage kernels of the 3D tetrahedral Maxwell operator for one (N, precision) (SURVEY.md §8(f)
+// row 4; the paper's hedge workload).
+//
+// Included once per translation unit (inst/k3_N<N>_<prec>.cu) with DG_N, DG_T, DG_TAG.
+// Fields (Hx, Hy, Hz, Ex, Ey, Ez), eps = mu = 1, PEC walls; the paper's two-kernel structure:
+//   K1 volume:  per 32-element tile (TMA-staged fields + geometry), dH/dt = -curl E, dE/dt = curl H
+//               by the chain rule d/dx = rx Dr + sx Ds + tx Dt regrouped so that each curl component
+//               is three mat-vecs: (curl E)_x = Dr(ry Ez - rz Ey) + Ds(sy Ez - sz Ey) + Dt(ty Ez - tz Ey)
+//               (18 mat-vecs per element); the operators broadcast from shared memory, one lane per
+//               element, warp g computing output rows [gR, gR + R)  -> rhsV
+//   K2 surface: per face point (split over the team) the traces q- (own node) and q+ (vmapP code;
+//               PEC mirror E+ = -E-, H+ = H-), the upwind flux 1/2 (n x [E] + a(n(n.[H]) - [H])) and
+//               1/2 (-n x [H] + a(n(n.[E]) - [E])) scaled by Fsc into shared memory; LIFT; + rhsV;
+//               the LSERK4 update (res = a res + dt rhs; q_out = q_in + b res) with coalesced stores.
+// Tile-blocked layout of kernel_api.h (6 fields, identity column swizzle).
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "kernel_api.h"
+#include "kernel3_api.h"
+
+#ifndef DG_N
+#error "DG_N must be defined"
+#endif
+#define DG_CAT2(a, b) a##b
+#define DG_CAT(a, b) DG_CAT2(a, b)
+
+namespace {
+
+using T = DG_T;
+constexpr bool F32 = sizeof(T) == 4;
+constexpr int N = DG_N;
+constexpr int NP = (N + 1) * (N + 2) * (N + 3) / 6;
+constexpr int NFP = (N + 1) * (N + 2) / 2;
+constexpr int NF = 4 * NFP;
+constexpr int TL = dg::TILE;
+constexpr int NG = dg::NGEO3;
+#ifndef DG_R
+#define DG_R (sizeof(DG_T) == 4 ? 8 : 4)
+#endif
+constexpr int R = DG_R;                    // output rows per warp
+constexpr int P = (NP + R - 1) / R;        // warps per tile
+constexpr int RP = P * R;                  // padded rows (zero operator rows)
+constexpr int TEAM = 32 * P;
+// operator block: DV[j][n] = {Dr, Ds, Dt, 0} [NP][RP], LV[m][n] [NF][RP], fmask [NF] int32
+struct alignas(4 * sizeof(T)) T4 { T x, y, z, w; };
+constexpr size_t DVB = (size_t)NP * RP * sizeof(T4);
+constexpr size_t LVB = (size_t)NF * RP * sizeof(T);
+constexpr size_t FMB = ((size_t)NF * 4 + 15) / 16 * 16;
+constexpr size_t OPS = DVB + LVB + FMB;
+constexpr size_t QB = (size_t)6 * NP * TL * sizeof(T);
+constexpr size_t GB = (size_t)NG * TL * sizeof(T);
+constexpr size_t SPB = (size_t)6 * NF * TL * sizeof(T);
+constexpr size_t BARB = 64;
+constexpr size_t SMEM_VOL = BARB + DVB + QB + GB;
+constexpr size_t SMEM_SURF = LVB + FMB + SPB;
+static_assert(SMEM_VOL <= 227 * 1024 && SMEM_SURF <= 227 * 1024, "3D kernel shared memory");
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile("{\n.reg .pred P1;\nW3_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W3_%=;\n}\n" ::"r"(
+                   smem_u32(bar)),
+               "r"(parity)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+template <int MODE>
+__host__ __device__ constexpr bool is_rk() { return MODE == dg::MODE_FUSED_RK || MODE == dg::MODE_SURFACE_RK; }
+
+// ---------------------------------------------------------------- K1: volume (curl) kernel
+__global__ void __launch_bounds__(TEAM, 1) volume3d(const dg::StageArgs3 p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  const T4* DV = reinterpret_cast<const T4*>(smem_raw + BARB);
+  T* sq = reinterpret_cast<T*>(smem_raw + BARB + DVB);
+  T* sg = reinterpret_cast<T*>(smem_raw + BARB + DVB + QB);
+  const T* __restrict__ q = static_cast<const T*>(p.q_in);
+  const T* __restrict__ geo = static_cast<const T*>(p.geo);
+  const int tid = threadIdx.x, g = tid >> 5, lane = tid & 31, n0 = g * R;
+  const int first = blockIdx.x, stride = gridDim.x;
+  const int n_it = first < p.ntiles ? (p.ntiles - first + stride - 1) / stride : 0;
+  if (n_it == 0) return;
+  auto issue = [&](int it) {
+    if (tid == 0) {
+      const int64_t t = first + (int64_t)it * stride;
+      mbar_expect_tx(bar, (unsigned)(QB + GB));
+#pragma unroll
+      for (int c = 0; c < 6; ++c)
+        tma_load_1d(sq + c * NP * TL, q + c * p.fstride + t * NP * TL, (unsigned)(NP * TL * sizeof(T)), bar);
+      tma_load_1d(sg, geo + t * NG * TL, (unsigned)GB, bar);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  {
+    const int4* src = reinterpret_cast<const int4*>(p.ops);
+    int4* dst = reinterpret_cast<int4*>(smem_raw + BARB);
+    for (int i = tid; i < (int)(DVB / 16); i += TEAM) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  issue(0);
+  for (int it = 0; it < n_it; ++it) {
+    mbar_wait(bar, (unsigned)(it & 1));
+    __syncthreads();
+    if (it + 1 < n_it && tid == 0) {
+      const int64_t t1 = first + (int64_t)(it + 1) * stride;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) prefetch_l2(q + c * p.fstride + t1 * NP * TL, (unsigned)(NP * TL * sizeof(T)));
+      prefetch_l2(geo + t1 * NG * TL, (unsigned)GB);
+    }
+    const int64_t t = first + (int64_t)it * stride;
+    const T* gg = sg + lane;
+    const T rx = gg[0 * TL], ry = gg[1 * TL], rz = gg[2 * TL], sx = gg[3 * TL], sy = gg[4 * TL], sz = gg[5 * TL],
+            tx = gg[6 * TL], ty = gg[7 * TL], tz = gg[8 * TL];
+    T acc[6][R];
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[c][r] = T(0);
+#pragma unroll 2
+    for (int j = 0; j < NP; ++j) {
+      const T* col = sq + j * TL + lane;
+      const T Hx = col[0 * NP * TL], Hy = col[1 * NP * TL], Hz = col[2 * NP * TL];
+      const T Ex = col[3 * NP * TL], Ey = col[4 * NP * TL], Ez = col[5 * NP * TL];
+      // (curl F)_x = sum_d D_d (dy_d Fz - dz_d Fy), _y = D_d(dz_d Fx - dx_d Fz), _z = D_d(dx_d Fy - dy_d Fx)
+      // with (dx_d, dy_d, dz_d) = (rx, ry, rz), (sx, sy, sz), (tx, ty, tz) for d = r, s, t
+      T W[6][3];
+      const T dxv[3] = {rx, sx, tx}, dyv[3] = {ry, sy, ty}, dzv[3] = {rz, sz, tz};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        W[0][d] = dyv[d] * Ez - dzv[d] * Ey;  // curl E -> accumulated, negated for dH/dt
+        W[1][d] = dzv[d] * Ex - dxv[d] * Ez;
+        W[2][d] = dxv[d] * Ey - dyv[d] * Ex;
+        W[3][d] = dyv[d] * Hz - dzv[d] * Hy;  // curl H -> dE/dt
+        W[4][d] = dzv[d] * Hx - dxv[d] * Hz;
+        W[5][d] = dxv[d] * Hy - dyv[d] * Hx;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const T4 d = DV[j * RP + n0 + r];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) acc[c][r] = fma(d.x, W[c][0], fma(d.y, W[c][1], fma(d.z, W[c][2], acc[c][r])));
+      }
+    }
+    __syncthreads();  // every warp is done with the tile's fields: the next TMA may overwrite them
+    if (it + 1 < n_it) issue(it + 1);
+    T* __restrict__ out = static_cast<T*>(p.out);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int n = n0 + r;
+      if (RP != NP && n >= NP) break;
+      const int64_t o = (t * NP + n) * TL + lane;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) out[c * p.vstride + o] = c < 3 ? -acc[c][r] : acc[c][r];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K2: surface + LIFT (+ LSERK4)
+template <int MODE>
+__global__ void __launch_bounds__(TEAM, 1) surface3d(const dg::StageArgs3 p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const T* LV = reinterpret_cast<const T*>(smem_raw);
+  const int32_t* fmask = reinterpret_cast<const int32_t*>(smem_raw + LVB);
+  T* sp = reinterpret_cast<T*>(smem_raw + LVB + FMB);
+  const T* __restrict__ q = static_cast<const T*>(p.q_in);
+  const T* __restrict__ geo = static_cast<const T*>(p.geo);
+  const int tid = threadIdx.x, g = tid >> 5, lane = tid & 31, n0 = g * R;
+  const int first = blockIdx.x, stride = gridDim.x;
+  const int n_it = first < p.ntiles ? (p.ntiles - first + stride - 1) / stride : 0;
+  if (n_it == 0) return;
+  {
+    const int4* src = reinterpret_cast<const int4*>(static_cast<const unsigned char*>(p.ops) + DVB);
+    int4* dst = reinterpret_cast<int4*>(smem_raw);
+    for (int i = tid; i < (int)((LVB + FMB) / 16); i += TEAM) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  const T alpha = static_cast<T>(p.alpha);
+  const bool read_res = is_rk<MODE>() && p.a != 0.0;
+  for (int it = 0; it < n_it; ++it) {
+    const int64_t t = first + (int64_t)it * stride;
+    const T* gg = geo + t * NG * TL + lane;
+    const int32_t* codes = p.vmapP + t * NF * TL + lane;
+    const T* qt = q + t * NP * TL + lane;
+    // flux at this warp's face points m = g, g + P, ...
+    for (int m = g; m < NF; m += P) {
+      const int f = m / NFP;
+      const int fm = fmask[m];
+      const T nx = __ldg(gg + (9 + 4 * f) * TL), ny = __ldg(gg + (10 + 4 * f) * TL), nz = __ldg(gg + (11 + 4 * f) * TL);
+      const T hF = __ldg(gg + (12 + 4 * f) * TL), bsc = __ldg(gg + (25 + f) * TL);
+      const int32_t code = __ldg(codes + m * TL);
+      T d[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        const T own = __ldg(qt + c * p.fstride + fm * TL);
+        const T nb = __ldg(q + c * p.fstride + code);
+        // PEC (bsc = -1, code = own node): H+ = H- ([H] = 0), E+ = -E- ([E] = 2 E-)
+        d[c] = c < 3 ? (bsc < T(0) ? T(0) : own - nb) : own - bsc * nb;
+      }
+      const T ndH = nx * d[0] + ny * d[1] + nz * d[2];
+      const T ndE = nx * d[3] + ny * d[4] + nz * d[5];
+      T* s = sp + m * TL + lane;
+      s[0 * NF * TL] = hF * ((ny * d[5] - nz * d[4]) + alpha * (nx * ndH - d[0]));
+      s[1 * NF * TL] = hF * ((nz * d[3] - nx * d[5]) + alpha * (ny * ndH - d[1]));
+      s[2 * NF * TL] = hF * ((nx * d[4] - ny * d[3]) + alpha * (nz * ndH - d[2]));
+      s[3 * NF * TL] = hF * (-(ny * d[2] - nz * d[1]) + alpha * (nx * ndE - d[3]));
+      s[4 * NF * TL] = hF * (-(nz * d[0] - nx * d[2]) + alpha * (ny * ndE - d[4]));
+      s[5 * NF * TL] = hF * (-(nx * d[1] - ny * d[0]) + alpha * (nz * ndE - d[5]));
+    }
+    __syncthreads();
+    T acc[6][R];
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[c][r] = T(0);
+#pragma unroll 2
+    for (int m = 0; m < NF; ++m) {
+      T fv[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) fv[c] = sp[(c * NF + m) * TL + lane];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const T l = LV[m * RP + n0 + r];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) acc[c][r] = fma(l, fv[c], acc[c][r]);
+      }
+    }
+    __syncthreads();  // sp is rewritten by the next tile
+    const T a = static_cast<T>(p.a), b = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int n = n0 + r;
+      if (RP != NP && n >= NP) break;
+      const int64_t o = (t * NP + n) * TL + lane;
+      T rhs[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        rhs[c] = acc[c][r];
+        if (MODE != dg::MODE_SURFACE) rhs[c] += static_cast<const T*>(p.rhsv)[c * p.vstride + o];
+      }
+      if constexpr (is_rk<MODE>()) {
+        T* __restrict__ res = static_cast<T*>(p.res);
+        T* __restrict__ qo = static_cast<T*>(p.q_out);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          T rs = dt * rhs[c];
+          if (read_res) rs = fma(a, __ldcs(res + c * p.vstride + o), rs);
+          if (p.write_res) __stcs(res + c * p.vstride + o, rs);
+          __stcs(qo + c * p.fstride + o, fma(b, rs, q[c * p.fstride + o]));
+        }
+      } else {
+        T* __restrict__ out = static_cast<T*>(p.out);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) out[c * p.vstride + o] = rhs[c];
+      }
+    }
+  }
+}
+
+template <typename KER>
+cudaError_t launch_k(KER kernel, size_t smem, const dg::StageArgs3& a, cudaStream_t s, int* cap) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 64) return cudaErrorInvalidDevice;
+  if (cap[dev] == 0) {
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cudaGetLastError(), e;
+    int per_sm = 0, sms = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TEAM, smem)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    cap[dev] = (per_sm > 0 ? per_sm : 1) * sms;
+  }
+  int grid = a.ntiles < cap[dev] ? a.ntiles : cap[dev];
+  if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
+  if (grid <= 0) return cudaSuccess;
+  kernel<<<grid, TEAM, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch(int mode, const dg::StageArgs3& a, cudaStream_t s) {
+  static int cap_v[64] = {0}, cap_rk[64] = {0}, cap_rhs[64] = {0}, cap_s[64] = {0};
+  switch (mode) {
+    case dg::MODE_VOLUME: return launch_k(volume3d, SMEM_VOL, a, s, cap_v);
+    case dg::MODE_SURFACE_RK: return launch_k(surface3d<dg::MODE_SURFACE_RK>, SMEM_SURF, a, s, cap_rk);
+    case dg::MODE_RHS: return launch_k(surface3d<dg::MODE_RHS>, SMEM_SURF, a, s, cap_rhs);
+    case dg::MODE_SURFACE: return launch_k(surface3d<dg::MODE_SURFACE>, SMEM_SURF, a, s, cap_s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+size_t ops_bytes() { return OPS; }
+void pack_ops(const double* Dr, const double* Ds, const double* Dt, const double* LIFT, const int* Fmask, void* out) {
+  unsigned char* o = static_cast<unsigned char*>(out);
+  for (size_t i = 0; i < OPS; ++i) o[i] = 0;
+  T4* dv = reinterpret_cast<T4*>(o);
+  for (int j = 0; j < NP; ++j)
+    for (int n = 0; n < NP; ++n) {
+      T4& e = dv[j * RP + n];
+      e.x = static_cast<T>(Dr[n * NP + j]);
+      e.y = static_cast<T>(Ds[n * NP + j]);
+      e.z = static_cast<T>(Dt[n * NP + j]);
+    }
+  T* lv = reinterpret_cast<T*>(o + DVB);
+  for (int m = 0; m < NF; ++m)
+    for (int n = 0; n < NP; ++n) lv[m * RP + n] = static_cast<T>(LIFT[n * NF + m]);
+  int32_t* fm = reinterpret_cast<int32_t*>(o + DVB + LVB);
+  for (int m = 0; m < NF; ++m) fm[m] = Fmask[m];
+}
+
+dg::KernelInfo3 info() {
+  dg::KernelInfo3 k;
+  k.N = N;
+  k.prec = (int)sizeof(T);
+  k.threads = TEAM;
+  k.rows_per_warp = R;
+  k.smem_volume = SMEM_VOL;
+  k.smem_surface = SMEM_SURF;
+  return k;
+}
+
+}  // namespace
+
+namespace dg {
+KernelModule3 DG_CAT(dg_module3_, DG_TAG)() {
+  KernelModule3 m;
+  m.N = N;
+  m.prec = (int)sizeof(T);
+  m.ops_bytes = &ops_bytes;
+  m.pack_ops = &pack_ops;
+  m.launch = &launch;
+  m.info = &info;
+  return m;
+}
+}  // namespace dg

@@ -50,6 +50,14 @@ dg_status set_err(dg_status s, const std::string& m) {
   return s;
 }
 
+}  // namespace
+
+namespace dg {
+void set_last_error(const std::string& m) { g_err = m; }  // the 3D calls (runtime3d.cu) report here too
+}  // namespace dg
+
+namespace {
+
 // LSERK4 (Carpenter-Kennedy 5-stage, 4th order; reading A10)
 const double kRKa[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
                         -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};

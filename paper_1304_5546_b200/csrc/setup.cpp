@@ -30,8 +30,8 @@
 namespace dg {
 
 namespace {
-
 [[noreturn]] void fail(int st, const std::string& m) { throw SetupError{st, m}; }
+}  // namespace
 
 // ---------------------------------------------------------------- 1D polynomials
 // Orthonormal Jacobi polynomial P_n^{(a,b)} at x[0..nx) (three-term recurrence).
@@ -62,8 +62,6 @@ void gradJacobiP(const double* x, int nx, double a, double b, int n, double* out
   const double f = std::sqrt(n * (n + a + b + 1.0));
   for (int i = 0; i < nx; ++i) out[i] *= f;
 }
-
-}  // namespace
 
 // Eigenvalues of a symmetric tridiagonal matrix (diag d[n], off-diag e[n-1]) by
 // Sturm-sequence bisection; ascending.
@@ -125,8 +123,6 @@ void lu_solve(int n, std::vector<double> A, int nrhs, std::vector<double>& B) {
   }
 }
 
-namespace {
-
 // Gauss nodes of P^{(a,b)}_{n+1} (Golub-Welsch; J_00 := 0 when a+b = 0).
 std::vector<double> jacobiGQ(double a, double b, int n) {
   if (n == 0) return {-(a - b) / (a + b + 2)};
@@ -163,8 +159,11 @@ std::vector<double> vandermonde1D(int n, const std::vector<double>& r) {
   return V;
 }
 
+namespace {
 const double kAlphaOpt[15] = {0.0000, 0.0000, 1.4152, 0.1001, 0.2751, 0.9800, 1.0999, 1.2832,
                               1.3648, 1.4773, 1.4959, 1.5743, 1.5770, 1.6223, 1.6258};
+
+}  // namespace
 
 // Edge warp of the warp-and-blend construction.
 std::vector<double> warpfactor(int n, const std::vector<double>& rout) {
@@ -193,6 +192,7 @@ std::vector<double> warpfactor(int n, const std::vector<double>& rout) {
   return warp;
 }
 
+namespace {
 void nodes2D(int n, std::vector<double>& r, std::vector<double>& s) {
   const double alpha = n < 16 ? kAlphaOpt[n - 1] : 5.0 / 3.0;
   const int Np = (n + 1) * (n + 2) / 2;
@@ -233,6 +233,8 @@ void nodes2D(int n, std::vector<double>& r, std::vector<double>& s) {
   }
 }
 
+}  // namespace
+
 // Orthonormal simplex mode phi_ij and its gradient at (r, s) via collapsed (a, b).
 void simplex_mode(const std::vector<double>& r, const std::vector<double>& s, int i, int j, double* phi,
                   double* dr, double* ds) {
@@ -266,8 +268,6 @@ void simplex_mode(const std::vector<double>& r, const std::vector<double>& s, in
     }
   }
 }
-
-}  // namespace
 
 RefElem build_refelem(int N) {
   if (N < 1 || N > 15) fail(DG_E_DEGREE, "degree N must be in [1, 15]");

@@ -71,6 +71,17 @@ void face_maps(const RefElem& ref, const Mesh& m, int64_t kl, int64_t* vmapM, in
 // Physical node coordinates of a global element.
 void element_nodes(const RefElem& ref, const Mesh& m, int64_t k, double* x, double* y);
 
+// Polynomial building blocks (setup.cpp), shared by the 2D and 3D (setup3d.cpp) reference elements.
+void jacobiP(const double* x, int nx, double a, double b, int n, double* out);      // orthonormal P_n^(a,b)
+void gradJacobiP(const double* x, int nx, double a, double b, int n, double* out);
+std::vector<double> jacobiGQ(double a, double b, int n);    // Gauss nodes (Sturm bisection)
+std::vector<double> jacobiGL(double a, double b, int n);    // Gauss-Lobatto nodes
+std::vector<double> vandermonde1D(int n, const std::vector<double>& r);
+std::vector<double> warpfactor(int n, const std::vector<double>& rout);  // edge warp / (1 - r^2), 0 at the ends
+// orthonormal triangle mode phi_ij (and d/dr, d/ds) at points (r, s); any output may be NULL
+void simplex_mode(const std::vector<double>& r, const std::vector<double>& s, int i, int j, double* phi,
+                  double* dr, double* ds);
+
 // Small dense linear algebra (row-major), exposed for the unit tests of the library.
 void lu_solve(int n, std::vector<double> A, int nrhs, std::vector<double>& B);  // A X = B, B [n][nrhs]
 std::vector<double> sym_tridiag_eigenvalues(const std::vector<double>& d, const std::vector<double>& e);
