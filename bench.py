@@ -530,6 +530,105 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- 3D (hedge)
+def bytes_3d(Np, Nfp, s, kind):
+    """Algorithmic bytes per element per stage of the 3D kernels: volume = read the
+    6 fields + 9 geometry words, write rhsV; surface = read rhsV, q (RK) and the residual on stages
+    1-4, write q_out and the residual on stages 0-3, + 20 face words + 4 Nfp neighbour codes (the
+    traces are re-reads of q: L2 hits, not counted)."""
+    if kind == "volume":
+        return (12 * Np + 9) * s
+    return (12 * Np + 2 * 0.8 * 6 * Np + 20) * s + 4 * Nfp * 4
+
+
+def flops_3d(N, kind):
+    Np, Nfp = (N + 1) * (N + 2) * (N + 3) // 6, (N + 1) * (N + 2) // 2
+    if kind == "volume":
+        return 2 * 18 * Np * Np + 36 * 2 * Np   # 18 mat-vecs + the chain-rule combinations
+    NF = 4 * Nfp
+    return 2 * 6 * Np * NF + NF * 6 * 12 + 6 * Np * 5  # LIFT of 6 fields + flux + rhsV add and LSERK4
+
+
+def run_3d(args):
+    """The 3D tetrahedral Maxwell step (config 'hedge3d'): PEC unit cube, n^3 cells x 6 Kuhn tetrahedra,
+    the (1,1,1) cavity mode, LSERK4; one step = 5 stages x (volume kernel + surface/LIFT/RK kernel)."""
+    import torch
+
+    from paper_1304_5546_b200 import dg3
+
+    torch.cuda.set_device(0)
+    N, n, prec = args.order, args.n, args.prec
+    VX, VY, VZ, E = dginputs.cube_tet_mesh(n)
+    K = E.shape[0]
+    c = dg3.dg3_setup(N, VX, VY, VZ, E, precision=prec)
+    Np, Nfp = c.Np, c.Nfp
+    x, y, z = c.nodes()
+    c.set_fields(*dginputs.cube_cavity_mode(x, y, z, 0.0))
+    dt = dginputs.cfl_dt_3d(VX, VY, VZ, E, N)
+    stream = torch.cuda.ExternalStream(c.stream())
+    c.run(dt, args.warmup)
+    c.sync()
+    c.profile(True)
+    c.profile(False)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(physical_gpu(0)) as clk:
+        t0 = time.perf_counter()
+        e0.record(stream)
+        c.run(dt, args.steps)
+        e1.record(stream)
+        e1.synchronize()
+        t1 = time.perf_counter()
+    ms = e0.elapsed_time(e1)
+    launches = sum(v["launches"] for v in c.kernel_stats().values())
+    prof = min(args.steps, 10)
+    c.profile(True)
+    c.run(dt, prof)
+    st = c.kernel_stats()
+    c.profile(False)
+    c.sync()
+    hbm, peak_src = peaks()
+    s = prec
+    roofs = {}
+    for kind in ("volume", "surface"):
+        k_ms = st[kind]["ms"] / (5 * prof)
+        ab = bytes_3d(Np, Nfp, s, kind) * K
+        fl = flops_3d(N, kind) * K
+        cb, cp, csrc = compute_peak(s, "fma")
+        gbs, tfl = ab / (k_ms * 1e-3) / 1e9, fl / (k_ms * 1e-3) / 1e12
+        hroof = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "peak_source": peak_src}
+        croof = {"bound": cb, "achieved": tfl, "peak": cp, "unit": "TFLOP/s", "frac": tfl / cp, "peak_source": csrc}
+        main, alt = (croof, hroof) if fl / ab > cp * 1e3 / hbm else (hroof, croof)
+        roofs[kind] = dict(main, kernel=f"{kind}3d", avg_launch_ms=k_ms, algorithmic_bytes_per_launch=ab,
+                           flops_per_launch=fl, achieved_gflops=tfl * 1e3,
+                           other_roof={k: alt[k] for k in ("bound", "achieved", "peak", "unit", "frac")})
+    dom = max(roofs, key=lambda k: roofs[k]["avg_launch_ms"])
+    roof = dict(roofs[dom], second_kernel=roofs["volume" if dom == "surface" else "surface"])
+    # e2e through the public API: set fields (host fp64), K steps, get fields
+    host = [np.ascontiguousarray(a) for a in dginputs.cube_cavity_mode(x, y, z, 0.0)]
+    t0e = time.perf_counter()
+    c.set_fields(*host)
+    c.run(dt, args.steps)
+    c.get_fields()
+    e2e_s = time.perf_counter() - t0e
+    c.destroy()
+    value = Np * K * 6 * 5 * args.steps / (ms * 1e-3)
+    fbytes = 6 * K * Np * 8
+    flops_step = 5 * K * (flops_3d(N, "volume") + flops_3d(N, "surface"))
+    line = {"metric": METRIC + " [3D tetrahedral path]", "value": value, "unit": UNIT + " (6 fields)", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "none", "vs_baseline": None, "dtype": "f32" if prec == 4 else "f64", "data": "synthetic",
+            "config": {"workload": f"hedge3d: 3D TM/TE Maxwell PEC unit cube, N={N}, K={K:,} tetrahedra "
+                                   f"({n}^3 cells x 6), {'fp32' if prec == 4 else 'fp64'}, LSERK4, cavity mode (1,1,1)",
+                       "N": N, "K": K, "Np": Np, "kernels": "volume (18 mat-vecs) + surface/LIFT/LSERK4 (FMA)",
+                       "l2": f"no flush: working set {(9 * K * Np * s) / 1e6:.0f} MB"},
+            "gflops": flops_step / (ms / args.steps * 1e-3) / 1e9,
+            "roofline": roof, "cpu_baseline": None,
+            "e2e": {"value": Np * K * 6 * 5 * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": fbytes / args.steps,
+                    "d2h_bytes_per_step": fbytes / args.steps},
+            "gpu_launches": launches, "clocks": clk.summary(t0, t1)}
+    print(json.dumps(line), flush=True)
+
+
 def spawn_ranks(n):
     """bench.py --gpus N without a launcher: re-run this command under torchrun, one rank per GPU
     (the driver's own launch line: --nnodes=1 --master-addr 127.0.0.1)."""
@@ -611,10 +710,17 @@ def main():
     ap.add_argument("--ref-n", type=int, default=48, help="oracle sample mesh cells per side")
     ap.add_argument("--ref-steps", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dim", type=int, default=2, choices=[2, 3],
+                    help="3: the 3D tetrahedral path (config hedge3d: --order N, --n cells per cube side)")
     ap.add_argument("--partitions", type=int, default=0,
                     help="dry run of the multi-GPU data path on ONE GPU: P in-process partitions "
                          "(transport 1, dg_run_group)")
     args = ap.parse_args()
+    if args.dim == 3:
+        args.config = "hedge3d"
+        args.order = args.order or 4
+        args.n = args.n or 40
+        args.prec = args.prec or 4
     preset = CONFIGS.get(args.config, CONFIGS["c4"])
     for key, val in preset.items():
         if getattr(args, key) is None:
@@ -636,6 +742,9 @@ def main():
         return
     if args.partitions > 0:
         run_partitions_dry(args)
+        return
+    if args.dim == 3:
+        run_3d(args)
         return
     if world > 1:
         import torch

@@ -43,10 +43,19 @@ constexpr int R = DG_R;                    // output rows per warp
 constexpr int P = (NP + R - 1) / R;        // warps per tile
 constexpr int RP = P * R;                  // padded rows (zero operator rows)
 constexpr int TEAM = 32 * P;
+// surface kernel: its own rows per warp (smaller: more warps to hide the trace-load latency)
+#ifndef DG_RS
+#define DG_RS (sizeof(DG_T) == 4 ? 4 : 2)
+#endif
+constexpr int RS = DG_RS;
+constexpr int PS = (NP + RS - 1) / RS;
+constexpr int RPS = PS * RS;
+constexpr int TEAMS = 32 * PS;
+constexpr int KPT = (NF + PS - 1) / PS;    // face points per warp (surface kernel)
 // operator block: DV[j][n] = {Dr, Ds, Dt, 0} [NP][RP], LV[m][n] [NF][RP], fmask [NF] int32
 struct alignas(4 * sizeof(T)) T4 { T x, y, z, w; };
 constexpr size_t DVB = (size_t)NP * RP * sizeof(T4);
-constexpr size_t LVB = (size_t)NF * RP * sizeof(T);
+constexpr size_t LVB = (size_t)NF * RPS * sizeof(T);
 constexpr size_t FMB = ((size_t)NF * 4 + 15) / 16 * 16;
 constexpr size_t OPS = DVB + LVB + FMB;
 constexpr size_t QB = (size_t)6 * NP * TL * sizeof(T);
@@ -176,21 +185,21 @@ __global__ void __launch_bounds__(TEAM, 1) volume3d(const dg::StageArgs3 p) {
 
 // ---------------------------------------------------------------- K2: surface + LIFT (+ LSERK4)
 template <int MODE>
-__global__ void __launch_bounds__(TEAM, 1) surface3d(const dg::StageArgs3 p) {
+__global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const T* LV = reinterpret_cast<const T*>(smem_raw);
   const int32_t* fmask = reinterpret_cast<const int32_t*>(smem_raw + LVB);
   T* sp = reinterpret_cast<T*>(smem_raw + LVB + FMB);
   const T* __restrict__ q = static_cast<const T*>(p.q_in);
   const T* __restrict__ geo = static_cast<const T*>(p.geo);
-  const int tid = threadIdx.x, g = tid >> 5, lane = tid & 31, n0 = g * R;
+  const int tid = threadIdx.x, g = tid >> 5, lane = tid & 31, n0 = g * RS;
   const int first = blockIdx.x, stride = gridDim.x;
   const int n_it = first < p.ntiles ? (p.ntiles - first + stride - 1) / stride : 0;
   if (n_it == 0) return;
   {
     const int4* src = reinterpret_cast<const int4*>(static_cast<const unsigned char*>(p.ops) + DVB);
     int4* dst = reinterpret_cast<int4*>(smem_raw);
-    for (int i = tid; i < (int)((LVB + FMB) / 16); i += TEAM) dst[i] = __ldg(src + i);
+    for (int i = tid; i < (int)((LVB + FMB) / 16); i += TEAMS) dst[i] = __ldg(src + i);
   }
   __syncthreads();
   const T alpha = static_cast<T>(p.alpha);
@@ -200,21 +209,27 @@ __global__ void __launch_bounds__(TEAM, 1) surface3d(const dg::StageArgs3 p) {
     const T* gg = geo + t * NG * TL + lane;
     const int32_t* codes = p.vmapP + t * NF * TL + lane;
     const T* qt = q + t * NP * TL + lane;
-    // flux at this warp's face points m = g, g + P, ...
-    for (int m = g; m < NF; m += P) {
+    // flux at this warp's face points m = g + kP (compile-time trip count: the trace loads of
+    // several points are in flight together)
+#pragma unroll 4
+    for (int k = 0; k < KPT; ++k) {
+      const int m = g + k * PS;
+      if (m >= NF) break;
       const int f = m / NFP;
       const int fm = fmask[m];
-      const T nx = __ldg(gg + (9 + 4 * f) * TL), ny = __ldg(gg + (10 + 4 * f) * TL), nz = __ldg(gg + (11 + 4 * f) * TL);
-      const T hF = __ldg(gg + (12 + 4 * f) * TL), bsc = __ldg(gg + (25 + f) * TL);
       const int32_t code = __ldg(codes + m * TL);
-      T d[6];
+      T own[6], nb[6];
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
-        const T own = __ldg(qt + c * p.fstride + fm * TL);
-        const T nb = __ldg(q + c * p.fstride + code);
-        // PEC (bsc = -1, code = own node): H+ = H- ([H] = 0), E+ = -E- ([E] = 2 E-)
-        d[c] = c < 3 ? (bsc < T(0) ? T(0) : own - nb) : own - bsc * nb;
+        own[c] = __ldg(qt + c * p.fstride + fm * TL);
+        nb[c] = __ldg(q + c * p.fstride + code);
       }
+      const T nx = __ldg(gg + (9 + 4 * f) * TL), ny = __ldg(gg + (10 + 4 * f) * TL), nz = __ldg(gg + (11 + 4 * f) * TL);
+      const T hF = __ldg(gg + (12 + 4 * f) * TL), bsc = __ldg(gg + (25 + f) * TL);
+      T d[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c)  // PEC (bsc = -1, code = own node): [H] = 0, [E] = 2 E-
+        d[c] = c < 3 ? (bsc < T(0) ? T(0) : own[c] - nb[c]) : own[c] - bsc * nb[c];
       const T ndH = nx * d[0] + ny * d[1] + nz * d[2];
       const T ndE = nx * d[3] + ny * d[4] + nz * d[5];
       T* s = sp + m * TL + lane;
@@ -226,19 +241,19 @@ __global__ void __launch_bounds__(TEAM, 1) surface3d(const dg::StageArgs3 p) {
       s[5 * NF * TL] = hF * (-(nx * d[1] - ny * d[0]) + alpha * (nz * ndE - d[5]));
     }
     __syncthreads();
-    T acc[6][R];
+    T acc[6][RS];
 #pragma unroll
     for (int c = 0; c < 6; ++c)
 #pragma unroll
-      for (int r = 0; r < R; ++r) acc[c][r] = T(0);
+      for (int r = 0; r < RS; ++r) acc[c][r] = T(0);
 #pragma unroll 2
     for (int m = 0; m < NF; ++m) {
       T fv[6];
 #pragma unroll
       for (int c = 0; c < 6; ++c) fv[c] = sp[(c * NF + m) * TL + lane];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const T l = LV[m * RP + n0 + r];
+      for (int r = 0; r < RS; ++r) {
+        const T l = LV[m * RPS + n0 + r];
 #pragma unroll
         for (int c = 0; c < 6; ++c) acc[c][r] = fma(l, fv[c], acc[c][r]);
       }
@@ -246,9 +261,9 @@ __global__ void __launch_bounds__(TEAM, 1) surface3d(const dg::StageArgs3 p) {
     __syncthreads();  // sp is rewritten by the next tile
     const T a = static_cast<T>(p.a), b = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r < RS; ++r) {
       const int n = n0 + r;
-      if (RP != NP && n >= NP) break;
+      if (RPS != NP && n >= NP) break;
       const int64_t o = (t * NP + n) * TL + lane;
       T rhs[6];
 #pragma unroll
@@ -276,7 +291,7 @@ __global__ void __launch_bounds__(TEAM, 1) surface3d(const dg::StageArgs3 p) {
 }
 
 template <typename KER>
-cudaError_t launch_k(KER kernel, size_t smem, const dg::StageArgs3& a, cudaStream_t s, int* cap) {
+cudaError_t launch_k(KER kernel, size_t smem, int team, const dg::StageArgs3& a, cudaStream_t s, int* cap) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -285,24 +300,24 @@ cudaError_t launch_k(KER kernel, size_t smem, const dg::StageArgs3& a, cudaStrea
     e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cudaGetLastError(), e;
     int per_sm = 0, sms = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TEAM, smem)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, team, smem)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
     cap[dev] = (per_sm > 0 ? per_sm : 1) * sms;
   }
   int grid = a.ntiles < cap[dev] ? a.ntiles : cap[dev];
   if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
   if (grid <= 0) return cudaSuccess;
-  kernel<<<grid, TEAM, smem, s>>>(a);
+  kernel<<<grid, team, smem, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch(int mode, const dg::StageArgs3& a, cudaStream_t s) {
   static int cap_v[64] = {0}, cap_rk[64] = {0}, cap_rhs[64] = {0}, cap_s[64] = {0};
   switch (mode) {
-    case dg::MODE_VOLUME: return launch_k(volume3d, SMEM_VOL, a, s, cap_v);
-    case dg::MODE_SURFACE_RK: return launch_k(surface3d<dg::MODE_SURFACE_RK>, SMEM_SURF, a, s, cap_rk);
-    case dg::MODE_RHS: return launch_k(surface3d<dg::MODE_RHS>, SMEM_SURF, a, s, cap_rhs);
-    case dg::MODE_SURFACE: return launch_k(surface3d<dg::MODE_SURFACE>, SMEM_SURF, a, s, cap_s);
+    case dg::MODE_VOLUME: return launch_k(volume3d, SMEM_VOL, TEAM, a, s, cap_v);
+    case dg::MODE_SURFACE_RK: return launch_k(surface3d<dg::MODE_SURFACE_RK>, SMEM_SURF, TEAMS, a, s, cap_rk);
+    case dg::MODE_RHS: return launch_k(surface3d<dg::MODE_RHS>, SMEM_SURF, TEAMS, a, s, cap_rhs);
+    case dg::MODE_SURFACE: return launch_k(surface3d<dg::MODE_SURFACE>, SMEM_SURF, TEAMS, a, s, cap_s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -321,7 +336,7 @@ void pack_ops(const double* Dr, const double* Ds, const double* Dt, const double
     }
   T* lv = reinterpret_cast<T*>(o + DVB);
   for (int m = 0; m < NF; ++m)
-    for (int n = 0; n < NP; ++n) lv[m * RP + n] = static_cast<T>(LIFT[n * NF + m]);
+    for (int n = 0; n < NP; ++n) lv[m * RPS + n] = static_cast<T>(LIFT[n * NF + m]);
   int32_t* fm = reinterpret_cast<int32_t*>(o + DVB + LVB);
   for (int m = 0; m < NF; ++m) fm[m] = Fmask[m];
 }
