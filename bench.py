@@ -629,6 +629,16 @@ def run_3d(args):
     print(json.dumps(line), flush=True)
 
 
+def visible_gpus():
+    """Number of CUDA devices this process can see (0 without a driver)."""
+    try:
+        import torch
+
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
 def spawn_ranks(n):
     """bench.py --gpus N without a launcher: re-run this command under torchrun, one rank per GPU
     (the driver's own launch line: --nnodes=1 --master-addr 127.0.0.1)."""
@@ -681,7 +691,8 @@ def run_partitions_dry(args):
         c.destroy()
     line = {"metric": METRIC, "value": Np * K * 3 * 5 * args.steps / (ms * 1e-3), "unit": UNIT, "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "none (dry run)", "vs_baseline": None, "dtype": "f32" if args.prec == 4 else "f64",
+            "scaling": "none (dry run)", "dry_run": True, "vs_baseline": None,
+            "dtype": "f32" if args.prec == 4 else "f64",
             "data": "synthetic",
             "config": {"workload": name, "N": args.order, "K": K, "variant": "split" if args.split else "fused",
                        "parallelism": f"{P} in-process partitions on 1 GPU (transport 1: halo pack, device-copy "
@@ -725,8 +736,15 @@ def main():
     for key, val in preset.items():
         if getattr(args, key) is None:
             setattr(args, key, val)
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.partitions == 0:
-        spawn_ranks(args.gpus)  # does not return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.partitions == 0 and args.impl == "ours":
+        visible = visible_gpus()
+        if visible >= args.gpus:
+            spawn_ranks(args.gpus)  # does not return
+        # fewer GPUs than ranks (e.g. a 1-GPU development box): the labelled dry run of the same data
+        # path -- args.gpus in-process partitions on one GPU -- instead of ranks that cannot start
+        print(f"warning: --gpus {args.gpus} but {visible} GPU(s) visible: dry run with {args.gpus} in-process "
+              f"partitions on one GPU", file=sys.stderr)
+        args.partitions = args.gpus
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.config == "c5w" and args.n == CONFIGS["c5w"]["n"]:  # weak scaling: ~524k elements per GPU
         args.n = {1: 512, 2: 724, 4: 1024, 8: 1448}.get(world_env, int(round(512 * world_env ** 0.5)))

@@ -90,3 +90,15 @@ def test_cpu_baseline_all_cores_and_single_thread():
     assert cb["kind"] == "oracle" and cb["cores"] == (os.cpu_count() or 1) and cb["value"] > 0
     assert cb["single_thread"]["cores"] == 1 and cb["single_thread"]["value"] > 0
     assert "3x3" in cb["sample"]
+
+
+def test_gpus_without_enough_devices_falls_back_to_the_labelled_dry_run(monkeypatch):
+    """--gpus N with fewer visible GPUs runs the in-process partition dry run (not torchrun ranks)."""
+    called = {}
+    monkeypatch.setattr(bench, "visible_gpus", lambda: 1)
+    monkeypatch.setattr(bench, "spawn_ranks", lambda n: called.setdefault("spawn", n))
+    monkeypatch.setattr(bench, "run_partitions_dry", lambda a: called.setdefault("dry", a.partitions))
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "2", "--steps", "3"])
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    bench.main()
+    assert called == {"dry": 2}
