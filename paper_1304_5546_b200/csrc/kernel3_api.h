@@ -20,7 +20,8 @@ struct StageArgs3 {
   const void* rhsv;       // [6][vstride] volume term (K1 output, K2 input)
   void* out;              // [6][vstride]
   const void* geo;        // [ntiles][NGEO3][32]
-  const int32_t* vmapP;   // [ntiles][4 Nfp][32] global offsets (within a field) of the neighbour node
+  const int32_t* vmapP;   // [ntiles][4 Nfp][32] neighbour node: >= 0 offset within a global field;
+                          // < 0 (KernelModule3::staged) same tile, shared-memory offset -(1 + code)
   const void* ops;        // packed operators (KernelModule3::pack_ops)
   int64_t fstride, vstride;
   int32_t ntiles, write_res, max_ctas;
@@ -30,6 +31,7 @@ struct StageArgs3 {
 struct KernelInfo3 {
   int N, prec, threads, rows_per_warp;
   size_t smem_volume, smem_surface;
+  int staged;  // 1: the surface kernel stages the tile's fields in shared memory
 };
 
 struct KernelModule3 {
@@ -41,6 +43,9 @@ struct KernelModule3 {
   // MODE_SURFACE (K2 alone -> out)
   cudaError_t (*launch)(int mode, const StageArgs3& a, cudaStream_t s) = nullptr;
   KernelInfo3 (*info)() = nullptr;
+  // 1: the surface kernel stages the tile's fields in shared memory, so a neighbour node in the same
+  // 32-element tile is coded as a shared-memory offset: vmapP code = -(1 + n * 32 + lane)
+  int staged = 0;
 };
 
 const KernelModule3* find_module3(int N, int prec);

@@ -47,7 +47,7 @@ constexpr int TEAM = 32 * P;
 #ifndef DG_RS
 #define DG_RS (sizeof(DG_T) == 4 ? 4 : 2)
 #endif
-constexpr int RS = DG_RS;
+constexpr int RS = DG_RS * 32 >= NP ? DG_RS : (NP + 31) / 32;  // at most 32 warps per CTA
 constexpr int PS = (NP + RS - 1) / RS;
 constexpr int RPS = PS * RS;
 constexpr int TEAMS = 32 * PS;
@@ -63,7 +63,14 @@ constexpr size_t GB = (size_t)NG * TL * sizeof(T);
 constexpr size_t SPB = (size_t)6 * NF * TL * sizeof(T);
 constexpr size_t BARB = 64;
 constexpr size_t SMEM_VOL = BARB + DVB + QB + GB;
-constexpr size_t SMEM_SURF = LVB + FMB + SPB;
+// the surface kernel stages the tile's fields and geometry by TMA (own and same-tile neighbour traces
+// and q_in from shared memory) whenever that fits; else traces straight from global memory (L2)
+constexpr size_t SMEM_SURF_Q = BARB + LVB + FMB + SPB + QB + GB;
+#ifndef DG_SQ
+#define DG_SQ 1
+#endif
+constexpr bool STAGEQ = DG_SQ && SMEM_SURF_Q <= 227 * 1024;
+constexpr size_t SMEM_SURF = STAGEQ ? SMEM_SURF_Q : LVB + FMB + SPB;
 static_assert(SMEM_VOL <= 227 * 1024 && SMEM_SURF <= 227 * 1024, "3D kernel shared memory");
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -187,28 +194,59 @@ __global__ void __launch_bounds__(TEAM, 1) volume3d(const dg::StageArgs3 p) {
 template <int MODE>
 __global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const T* LV = reinterpret_cast<const T*>(smem_raw);
-  const int32_t* fmask = reinterpret_cast<const int32_t*>(smem_raw + LVB);
-  T* sp = reinterpret_cast<T*>(smem_raw + LVB + FMB);
+  constexpr size_t OFF = STAGEQ ? BARB : 0;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  const T* LV = reinterpret_cast<const T*>(smem_raw + OFF);
+  const int32_t* fmask = reinterpret_cast<const int32_t*>(smem_raw + OFF + LVB);
+  T* sp = reinterpret_cast<T*>(smem_raw + OFF + LVB + FMB);
+  T* sq = reinterpret_cast<T*>(smem_raw + OFF + LVB + FMB + SPB);       // STAGEQ: the tile's fields
+  T* sgeo = reinterpret_cast<T*>(smem_raw + OFF + LVB + FMB + SPB + QB);  // STAGEQ: its geometry
   const T* __restrict__ q = static_cast<const T*>(p.q_in);
   const T* __restrict__ geo = static_cast<const T*>(p.geo);
   const int tid = threadIdx.x, g = tid >> 5, lane = tid & 31, n0 = g * RS;
   const int first = blockIdx.x, stride = gridDim.x;
   const int n_it = first < p.ntiles ? (p.ntiles - first + stride - 1) / stride : 0;
   if (n_it == 0) return;
+  auto issue = [&](int it) {
+    if (STAGEQ && tid == 0) {
+      const int64_t t = first + (int64_t)it * stride;
+      mbar_expect_tx(bar, (unsigned)(QB + GB));
+#pragma unroll
+      for (int c = 0; c < 6; ++c)
+        tma_load_1d(sq + c * NP * TL, q + c * p.fstride + t * NP * TL, (unsigned)(NP * TL * sizeof(T)), bar);
+      tma_load_1d(sgeo, geo + t * NG * TL, (unsigned)GB, bar);
+    }
+  };
+  if (STAGEQ && tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   {
     const int4* src = reinterpret_cast<const int4*>(static_cast<const unsigned char*>(p.ops) + DVB);
-    int4* dst = reinterpret_cast<int4*>(smem_raw);
+    int4* dst = reinterpret_cast<int4*>(smem_raw + OFF);
     for (int i = tid; i < (int)((LVB + FMB) / 16); i += TEAMS) dst[i] = __ldg(src + i);
   }
   __syncthreads();
+  issue(0);
   const T alpha = static_cast<T>(p.alpha);
   const bool read_res = is_rk<MODE>() && p.a != 0.0;
   for (int it = 0; it < n_it; ++it) {
     const int64_t t = first + (int64_t)it * stride;
-    const T* gg = geo + t * NG * TL + lane;
+    if constexpr (STAGEQ) {
+      mbar_wait(bar, (unsigned)(it & 1));
+      __syncthreads();
+      if (it + 1 < n_it && tid == 0) {
+        const int64_t t1 = t + stride;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) prefetch_l2(q + c * p.fstride + t1 * NP * TL, (unsigned)(NP * TL * sizeof(T)));
+        prefetch_l2(geo + t1 * NG * TL, (unsigned)GB);
+      }
+    }
+    // geometry and own traces: shared memory (STAGEQ) or global; field stride FSQ of that source
+    const T* gg = STAGEQ ? sgeo + lane : geo + t * NG * TL + lane;
+    const T* qt = STAGEQ ? sq + lane : q + t * NP * TL + lane;
+    const int64_t FSQ = STAGEQ ? (int64_t)NP * TL : p.fstride;
     const int32_t* codes = p.vmapP + t * NF * TL + lane;
-    const T* qt = q + t * NP * TL + lane;
     // flux at this warp's face points m = g + kP (compile-time trip count: the trace loads of
     // several points are in flight together)
 #pragma unroll 4
@@ -218,14 +256,17 @@ __global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
       const int f = m / NFP;
       const int fm = fmask[m];
       const int32_t code = __ldg(codes + m * TL);
+      // code >= 0: offset in a global field; code < 0 (STAGEQ): same tile, shared offset -(1 + code)
+      const T* pn = code >= 0 ? q + code : sq + (-1 - code);
+      const int64_t fsn = code >= 0 ? p.fstride : (int64_t)NP * TL;
       T own[6], nb[6];
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
-        own[c] = __ldg(qt + c * p.fstride + fm * TL);
-        nb[c] = __ldg(q + c * p.fstride + code);
+        own[c] = qt[c * FSQ + fm * TL];
+        nb[c] = pn[c * fsn];
       }
-      const T nx = __ldg(gg + (9 + 4 * f) * TL), ny = __ldg(gg + (10 + 4 * f) * TL), nz = __ldg(gg + (11 + 4 * f) * TL);
-      const T hF = __ldg(gg + (12 + 4 * f) * TL), bsc = __ldg(gg + (25 + f) * TL);
+      const T nx = gg[(9 + 4 * f) * TL], ny = gg[(10 + 4 * f) * TL], nz = gg[(11 + 4 * f) * TL];
+      const T hF = gg[(12 + 4 * f) * TL], bsc = gg[(25 + f) * TL];
       T d[6];
 #pragma unroll
       for (int c = 0; c < 6; ++c)  // PEC (bsc = -1, code = own node): [H] = 0, [E] = 2 E-
@@ -279,12 +320,18 @@ __global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
           T rs = dt * rhs[c];
           if (read_res) rs = fma(a, __ldcs(res + c * p.vstride + o), rs);
           if (p.write_res) __stcs(res + c * p.vstride + o, rs);
-          __stcs(qo + c * p.fstride + o, fma(b, rs, q[c * p.fstride + o]));
+          __stcs(qo + c * p.fstride + o, fma(b, rs, qt[c * FSQ + n * TL]));
         }
       } else {
         T* __restrict__ out = static_cast<T*>(p.out);
 #pragma unroll
         for (int c = 0; c < 6; ++c) out[c * p.vstride + o] = rhs[c];
+      }
+    }
+    if constexpr (STAGEQ) {
+      if (it + 1 < n_it) {
+        __syncthreads();  // every thread is done with the tile's staged fields
+        issue(it + 1);
       }
     }
   }
@@ -349,6 +396,7 @@ dg::KernelInfo3 info() {
   k.rows_per_warp = R;
   k.smem_volume = SMEM_VOL;
   k.smem_surface = SMEM_SURF;
+  k.staged = STAGEQ ? 1 : 0;
   return k;
 }
 
@@ -363,6 +411,7 @@ KernelModule3 DG_CAT(dg_module3_, DG_TAG)() {
   m.pack_ops = &pack_ops;
   m.launch = &launch;
   m.info = &info;
+  m.staged = STAGEQ ? 1 : 0;
   return m;
 }
 }  // namespace dg

@@ -268,8 +268,10 @@ void host_geometry(dg3_ctx* c, std::vector<T>& g, std::vector<int32_t>& codes) {
     }
     for (int mm = 0; mm < NF; ++mm) {
       const int64_t gp = m.vmapP[k * NF + mm];
-      const int64_t k2 = gp / Np;
-      codes[(t * NF + mm) * 32 + lane] = (int32_t)blk(c->slot[k2], (int)(gp - k2 * Np));
+      const int64_t k2 = gp / Np, d2 = c->slot[k2];
+      const int n2 = (int)(gp - k2 * Np);
+      codes[(t * NF + mm) * 32 + lane] =
+          (c->km->staged && (d2 >> 5) == t) ? (int32_t)(-(1 + (int64_t)n2 * 32 + (d2 & 31))) : (int32_t)blk(d2, n2);
     }
   }
 }
