@@ -67,7 +67,16 @@ constexpr int TL = dg::TILE;
 #ifndef DG_MMA
 #define DG_MMA 0  // chosen per (N, precision) by tools/tune.py
 #endif
-constexpr bool USE_MMA = !F32 && (DG_MMA == 1 || DG_MMA == 2);
+constexpr bool USE_MMA = !F32 && (DG_MMA == 1 || DG_MMA == 2 || DG_MMA == 4);
+// DG_MMA=4 (fp64): the DMMA contractions split into (row group, n-tile) units -- PU warps per team (a
+// multiple of 4, so every SM sub-partition holds the same number of warps: with one team per SM and
+// PR = 6 row groups the one-row-group-per-warp team leaves two sub-partitions with twice the DMMAs of
+// the other two); warp w owns n-tile w % 4 and row groups w / 4 + i PU / 4, so the B fragments (fields)
+// it loads serve all of its units
+constexpr bool DMMA_U = !F32 && DG_MMA == 4;
+#ifndef DG_PU
+#define DG_PU 8
+#endif
 // fp32 only: the same contractions as 3xTF32 products on the tensor cores (mma.sync
 // m16n8k8: A = fields, elements x nodes; B = operator^T), split hi + lo so the result
 // keeps fp32 accuracy -- DG_MMA=1: one 16-element m-tile per warp, two warps per tile;
@@ -86,7 +95,11 @@ constexpr int PR = (NP + 7) / 8;                     // DMMA row groups (8 outpu
 #define DG_R (sizeof(DG_T) == 4 ? 8 : 6)
 #endif
 constexpr int R_TARGET = USE_MMA ? 8 : DG_R;  // max rows per warp
+static_assert(!DMMA_U || DG_PU % 4 == 0, "DG_PU: a multiple of 4 warps");
+constexpr int UST = DG_PU / 4;                     // DMMA_U: row-group stride between a warp's units
+constexpr int UW = DMMA_U ? (PR + UST - 1) / UST : 1;  // DMMA_U: units (row groups) per warp
 constexpr int P = USE_TF ? (TF_SPLIT ? 4 : 2)
+                          : DMMA_U ? DG_PU
                           : USE_MMA ? (DMMA_SPLIT ? 2 * PR : PR) : (NP + R_TARGET - 1) / R_TARGET;  // warps per tile
 constexpr int R = (NP + P - 1) / P;                // rows per warp
 constexpr int RP = P * R;                          // padded rows (extra rows are zero)
@@ -160,7 +173,7 @@ constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
 #ifndef DG_RT
 #define DG_RT 1
 #endif
-constexpr bool RES_TMA = USE_TF && DG_RT;
+constexpr bool RES_TMA = (USE_TF || DMMA_U) && DG_RT;
 // DG_FF: phase order of the fused kernels.  0: volume -> flux -> LIFT (the volume
 // accumulators stay live across the flux phase); 1: flux -> volume -> LIFT (nothing but the
 // face-point codes is live during the flux phase, so the peak register count drops)
@@ -168,16 +181,36 @@ constexpr bool RES_TMA = USE_TF && DG_RT;
 #define DG_FF 0
 #endif
 constexpr bool FLUX_FIRST = DG_FF;
+// DG_FF = 2 (DMMA_U tiles): flux first WITHOUT a barrier before the volume -- the barrier the LIFT needs
+// comes after the volume, so a warp's flux arithmetic and its volume DMMAs are one instruction stream
+// the scheduler can interleave (the flux fills issue slots while the DMMA pipe works)
+constexpr bool FLUX_FIRST_NB = DG_FF == 2;
 __host__ __device__ constexpr size_t slot_bytes(bool surf, bool mat, bool rk) {
   return QB + geo_bytes(mat) + (surf ? SPB : 0) + (RES_TMA && rk ? QB : 0);
 }
+// DG_WP (FMA path): the volume operands W1 = rx Hy - ry Hx, W2 = sx Hy - sy Hx are formed ONCE per tile
+// into a shared-memory buffer (every warp of the team splits the (node, element) pairs) instead of by
+// every warp for every column it consumes -- P times fewer of those products, and the volume loop
+// becomes pure loads + FMAs (4 per operator row and column)
+#ifndef DG_WP
+#define DG_WP 0
+#endif
+constexpr bool WPRE = DG_WP && DG_MMA == 0;
+// DG_GL (S = 3 pipeline): a tile's cross-tile neighbour gathers are issued at the tile's own start
+// (after its barrier) and each thread waits for its own cp.async groups right before its flux points
+// (the thread that gathers a point is the thread that forms its flux); with DG_GL = 0 they are issued
+// right after the previous tile's LIFT, where their queued copies hold up that tile's epilogue stores
+#ifndef DG_GL
+#define DG_GL 0
+#endif
 constexpr size_t BARB = 64;  // mbarriers: one per slot
+constexpr size_t WPB = WPRE ? (size_t)2 * NP * TL * sizeof(T) : 0;  // DG_WP buffer: W1, W2 [NP][32]
 // S = 3 is the split pipeline: two {q, geo} buffers (tile t+1's fields and geometry stream in
 // while t computes) and ONE {flux, residual} buffer, refilled in the tile's own flow (residual
 // by TMA at the start of the tile, next tile's neighbour gathers right after the LIFT).
 __host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat, bool rk) {
-  return S == 3 ? BARB + OPB_SMEM + 2 * (QB + geo_bytes(mat)) + (surf ? SPB : 0) + (RES_TMA && rk ? QB : 0)
-                : BARB + OPB_SMEM + S * slot_bytes(surf, mat, rk);
+  return WPB + (S == 3 ? BARB + OPB_SMEM + 2 * (QB + geo_bytes(mat)) + (surf ? SPB : 0) + (RES_TMA && rk ? QB : 0)
+                       : BARB + OPB_SMEM + S * slot_bytes(surf, mat, rk));
 }
 // Slots per team: 2 = double-buffered (tile t+1 streams in while t computes), 1 = latency
 // hidden across resident teams instead.  Measured at C4 (N=5): fp32 is issue-bound and
@@ -186,6 +219,7 @@ __host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat, bool
 #define DG_S (sizeof(DG_T) == 4 ? 1 : 2)
 #endif
 __host__ __device__ constexpr int nslots(bool, bool) { return DG_S; }
+constexpr bool GATHER_LATE = DG_GL && DG_S == 3;
 constexpr int CTAS_BY_SMEM = (int)((227 * 1024) / smem_total(nslots(true, false), true, false, true));
 #ifndef DG_C
 #define DG_C 5  // measured (C4 fp32): 5 teams x 128 registers beats 8 x 80 (spills) and 4 x 168
@@ -232,6 +266,8 @@ __device__ __forceinline__ void st_out(V* p, const V& v) {
 }
 constexpr int KLT_ = (NF + 7) / 8;
 constexpr int KCODE = FX ? 4 * KLT_ : KPT;  // codes per thread
+static_assert(!(FX && GATHER_LATE), "DG_GL is not implemented with DG_FX");
+static_assert(DG_FF != 2 || DMMA_U, "DG_FF = 2 is implemented for the DMMA_U tiles only");
 struct PointElem { int m, e; };
 __device__ __forceinline__ PointElem pair_of(int g, int lane, int k) {  // m = NF: no point
   if constexpr (FX) {
@@ -325,7 +361,8 @@ using LV_t = typename std::conditional<F32, float2, double>::type;
 // ---------------------------------------------------------------- phase A: volume
 template <typename DVT>  // DVT = DV_t (a template parameter so the other precision's branch is discarded)
 __device__ __forceinline__ void volume_rows(const T* __restrict__ sq, const DVT* __restrict__ DV, int n0, int lane,
-                                            T rx, T sx, T ry, T sy, T (&rhx)[R], T (&rhy)[R], T (&rez)[R]) {
+                                            T rx, T sx, T ry, T sy, T (&rhx)[R], T (&rhy)[R], T (&rez)[R],
+                                            const T* __restrict__ sw = nullptr) {
   T u[R], v[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) { u[r] = T(0); v[r] = T(0); rez[r] = T(0); }
@@ -334,11 +371,21 @@ __device__ __forceinline__ void volume_rows(const T* __restrict__ sq, const DVT*
     if constexpr (F32) {
       const int j0 = 2 * jc;
       const int j1 = (2 * jc + 1 < NP) ? 2 * jc + 1 : NP - 1;  // pad column has zero Dr/Ds
-      const T hx0 = sq[(0 * NP + j0) * TL + lane], hx1 = sq[(0 * NP + j1) * TL + lane];
-      const T hy0 = sq[(1 * NP + j0) * TL + lane], hy1 = sq[(1 * NP + j1) * TL + lane];
       const T ez0 = sq[(2 * NP + j0) * TL + lane], ez1 = sq[(2 * NP + j1) * TL + lane];
-      const T w10 = rx * hy0 - ry * hx0, w20 = sx * hy0 - sy * hx0;
-      const T w11 = rx * hy1 - ry * hx1, w21 = sx * hy1 - sy * hx1;
+      T w10, w20, w11, w21;
+      if constexpr (WPRE) {
+        w10 = sw[j0 * TL + lane];
+        w20 = sw[(NP + j0) * TL + lane];
+        w11 = sw[j1 * TL + lane];
+        w21 = sw[(NP + j1) * TL + lane];
+      } else {
+        const T hx0 = sq[(0 * NP + j0) * TL + lane], hx1 = sq[(0 * NP + j1) * TL + lane];
+        const T hy0 = sq[(1 * NP + j0) * TL + lane], hy1 = sq[(1 * NP + j1) * TL + lane];
+        w10 = rx * hy0 - ry * hx0;
+        w20 = sx * hy0 - sy * hx0;
+        w11 = rx * hy1 - ry * hx1;
+        w21 = sx * hy1 - sy * hx1;
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const DVT d = ldop(DV + jc * RP + n0 + r);
@@ -353,10 +400,17 @@ __device__ __forceinline__ void volume_rows(const T* __restrict__ sq, const DVT*
       }
     } else {
       const int j = jc;
-      const T hx = sq[(0 * NP + j) * TL + lane];
-      const T hy = sq[(1 * NP + j) * TL + lane];
       const T ez = sq[(2 * NP + j) * TL + lane];
-      const T w1 = rx * hy - ry * hx, w2 = sx * hy - sy * hx;
+      T w1, w2;
+      if constexpr (WPRE) {
+        w1 = sw[j * TL + lane];
+        w2 = sw[(NP + j) * TL + lane];
+      } else {
+        const T hx = sq[(0 * NP + j) * TL + lane];
+        const T hy = sq[(1 * NP + j) * TL + lane];
+        w1 = rx * hy - ry * hx;
+        w2 = sx * hy - sy * hx;
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const DVT d = ldop(DV + j * RP + n0 + r);
@@ -442,6 +496,7 @@ __device__ __forceinline__ void flux_one(const TT* __restrict__ sq, const TT* __
 template <bool MAT>
 __device__ __forceinline__ void flux_points(const T* __restrict__ sq, const T* __restrict__ gg, T* __restrict__ sp,
                                             const int32_t (&vmc)[KCODE], int g, int lane, T alpha) {
+  if constexpr (GATHER_LATE) cp_async_wait_all();  // this thread's own neighbour gathers (DG_GL)
   T fz[3][3];
   if constexpr (ZC && !MAT) zc_faces(gg, fz);
 #pragma unroll
@@ -977,6 +1032,177 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
   }
 }
 
+// One tile on the DMMA path split into (row group, n-tile) units (DG_MMA=4): warp g owns n-tile
+// nt = g % 4 (elements 8nt .. 8nt+7) and row groups rg_i = g / 4 + i UST (i < UW; rg_i >= PR: none).
+// Per k-step the warp loads the B fragments of its n-tile once (Ez, and W1, W2 formed from Hx, Hy)
+// and issues them against the A fragments (operator rows) of each of its row groups.  Same algebra as
+// mma_tile: u = Dr Ez, v = Ds Ez, w = Dr W1 + Ds W2 -> flux -> rhs += LIFT f -> 1/mu, 1/eps -> LSERK4.
+template <int MODE, bool MAT, typename TT, typename HOOK>
+__device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
+                                           TT* __restrict__ sp, const TT* __restrict__ sr,
+                                           const unsigned char* __restrict__ ops, const int32_t (&vmc)[KCODE],
+                                           int tile, int g, int lane, TT alpha, bool read_res, const HOOK& after_lift) {
+  using MT = ModeTraits<MODE>;
+  using V2 = double2;
+  const int nt = g & 3, rg0 = g >> 2;
+  auto rg_of = [&](int i) { return rg0 + i * UST; };
+  auto unit_ok = [&](int i) { return (UW - 1) * UST + (P / 4 - 1) < PR || rg_of(i) < PR; };  // compile-time when full
+  const int eb = 8 * nt + (lane >> 2);             // B-fragment element of this lane
+  const int ec0 = 8 * nt + 2 * (lane & 3);         // C-fragment elements ec0, ec0 + 1
+  if constexpr (FLUX_FIRST && MT::surf) {
+    flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
+    if constexpr (!FLUX_FIRST_NB) __syncthreads();
+  }
+  TT rhx[UW][2], rhy[UW][2], rez[UW][2];
+  if constexpr (MT::vol) {
+    const TT rxb = sg[0 * TL + eb], sxb = sg[1 * TL + eb], ryb = sg[2 * TL + eb], syb = sg[3 * TL + eb];
+    TT u[UW][2], v[UW][2], w2a[UW][2];
+#pragma unroll
+    for (int i = 0; i < UW; ++i) u[i][0] = u[i][1] = v[i][0] = v[i][1] = rez[i][0] = rez[i][1] = w2a[i][0] = w2a[i][1] = TT(0);
+    const V2* AV = reinterpret_cast<const V2*>(ops);
+#pragma unroll
+    for (int ks = 0; ks < KV; ++ks) {
+      const int j = 4 * ks + (lane & 3);
+      const int jc = j < NP ? j : NP - 1;  // padded k rows: A is zero there
+      const int addr = jc * TL + colx(jc, eb);
+      const TT ez = sq[2 * NP * TL + addr], hx = sq[addr], hy = sq[NP * TL + addr];
+      const TT w1 = rxb * hy - ryb * hx, w2 = sxb * hy - syb * hx;
+#pragma unroll
+      for (int i = 0; i < UW; ++i) {
+        if (!unit_ok(i)) continue;
+        const V2 a = ldop(AV + (ks * PR + rg_of(i)) * 32 + lane);
+        dmma(u[i][0], u[i][1], a.x, ez);
+        dmma(v[i][0], v[i][1], a.y, ez);
+        dmma(rez[i][0], rez[i][1], a.x, w1);
+        dmma(w2a[i][0], w2a[i][1], a.y, w2);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ec = ec0 + h;
+      const TT rx = sg[0 * TL + ec], sx = sg[1 * TL + ec], ry = sg[2 * TL + ec], sy = sg[3 * TL + ec];
+#pragma unroll
+      for (int i = 0; i < UW; ++i) {
+        rez[i][h] += w2a[i][h];
+        rhx[i][h] = -(ry * u[i][h] + sy * v[i][h]);
+        rhy[i][h] = rx * u[i][h] + sx * v[i][h];
+      }
+    }
+  } else if constexpr (MODE == dg::MODE_SURFACE_RK) {
+    const TT* __restrict__ rv = static_cast<const TT*>(p.rhsv);
+#pragma unroll
+    for (int i = 0; i < UW; ++i) {
+      if (!unit_ok(i)) continue;
+      const int n = 8 * rg_of(i) + (lane >> 2), nc = n < NP ? n : NP - 1;
+      const int64_t off = ((int64_t)tile * NP + nc) * TL + colx(nc, ec0);
+      const V2 x = *reinterpret_cast<const V2*>(rv + off);
+      const V2 y = *reinterpret_cast<const V2*>(rv + p.vstride + off);
+      const V2 z = *reinterpret_cast<const V2*>(rv + 2 * p.vstride + off);
+      rhx[i][0] = x.x; rhx[i][1] = x.y;
+      rhy[i][0] = y.x; rhy[i][1] = y.y;
+      rez[i][0] = z.x; rez[i][1] = z.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < UW; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) rhx[i][h] = rhy[i][h] = rez[i][h] = TT(0);
+  }
+  V2 rr[UW][3];  // LSERK4 residual pairs (in flight during the surface phase; RES_TMA: staged in sr)
+  if constexpr (MT::rk && !RES_TMA) {
+    if (read_res) {
+      const TT* __restrict__ res = static_cast<const TT*>(p.res);
+#pragma unroll
+      for (int i = 0; i < UW; ++i) {
+        if (!unit_ok(i)) continue;
+        const int n = 8 * rg_of(i) + (lane >> 2), nc = n < NP ? n : NP - 1;
+        const int64_t off = ((int64_t)tile * NP + nc) * TL + colx(nc, ec0);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) rr[i][c] = __ldcs(reinterpret_cast<const V2*>(res + c * p.vstride + off));
+      }
+    }
+  }
+  if constexpr (MT::surf) {
+    if constexpr (!FLUX_FIRST) {
+      flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
+      __syncthreads();
+    } else if constexpr (FLUX_FIRST_NB) {
+      __syncthreads();  // every warp's flux is in sp
+    }
+    const TT* AL = reinterpret_cast<const TT*>(ops + DVB);
+#pragma unroll
+    for (int ks = 0; ks < KL; ++ks) {
+      const int m = 4 * ks + (lane & 3);
+      const int mc = m < NF ? m : NF - 1;
+      const int addr = mc * TL + colx(mc, eb);
+      const TT f0 = sp[0 * NFE * TL + addr], f1 = sp[1 * NFE * TL + addr], f2 = sp[2 * NFE * TL + addr];
+#pragma unroll
+      for (int i = 0; i < UW; ++i) {
+        if (!unit_ok(i)) continue;
+        const TT a = ldop(AL + (ks * PR + rg_of(i)) * 32 + lane);
+        dmma(rhx[i][0], rhx[i][1], a, f0);
+        dmma(rhy[i][0], rhy[i][1], a, f1);
+        dmma(rez[i][0], rez[i][1], a, f2);
+      }
+    }
+  }
+  after_lift();
+  if constexpr (MAT) {
+    if (MODE != dg::MODE_VOLUME || p.scale_volume) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const TT imu = sg[16 * TL + ec0 + h], ieps = sg[17 * TL + ec0 + h];
+#pragma unroll
+        for (int i = 0; i < UW; ++i) {
+          rhx[i][h] *= imu;
+          rhy[i][h] *= imu;
+          rez[i][h] *= ieps;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < UW; ++i) {
+    if (!unit_ok(i)) continue;
+    const int n = 8 * rg_of(i) + (lane >> 2);
+    if (n >= NP) continue;
+    const int col = colx(n, ec0);
+    const int64_t off = ((int64_t)tile * NP + n) * TL + col;
+    const TT r3[3][2] = {{rhx[i][0], rhx[i][1]}, {rhy[i][0], rhy[i][1]}, {rez[i][0], rez[i][1]}};
+    if constexpr (MT::rk) {
+      TT* __restrict__ res = static_cast<TT*>(p.res);
+      TT* __restrict__ qo = static_cast<TT*>(p.q_out);
+      const TT a = static_cast<TT>(p.a), b = static_cast<TT>(p.b), dt = static_cast<TT>(p.dt);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        V2 rs;
+        rs.x = dt * r3[c][0];
+        rs.y = dt * r3[c][1];
+        if (read_res) {
+          const V2 ro = RES_TMA ? *reinterpret_cast<const V2*>(sr + (c * NP + n) * TL + col) : rr[i][c];
+          rs.x = fma(a, ro.x, rs.x);
+          rs.y = fma(a, ro.y, rs.y);
+        }
+        if (p.write_res) st_out(reinterpret_cast<V2*>(res + c * p.vstride + off), rs);
+        const V2 qi = *reinterpret_cast<const V2*>(sq + (c * NP + n) * TL + col);
+        V2 qn;
+        qn.x = fma(b, rs.x, qi.x);
+        qn.y = fma(b, rs.y, qi.y);
+        st_out(reinterpret_cast<V2*>(qo + c * p.fstride + off), qn);
+      }
+    } else {
+      TT* __restrict__ out = static_cast<TT*>(p.out);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        V2 o;
+        o.x = r3[c][0];
+        o.y = r3[c][1];
+        *reinterpret_cast<V2*>(out + c * p.vstride + off) = o;
+      }
+    }
+  }
+}
+
 // Persistent, software-pipelined stage kernel (one team per CTA).
 template <int MODE, bool MAT>
 __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageArgs p) {
@@ -1000,6 +1226,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   const DV_t* DV = reinterpret_cast<const DV_t*>(opbase);
   const LV_t* LV = reinterpret_cast<const LV_t*>(opbase + DVB);
   unsigned char* slots = smem_raw + BARB + OPB_SMEM;
+  T* const sw = reinterpret_cast<T*>(smem_raw + smem_total(S, MT::surf, MAT, MT::rk) - WPB);  // DG_WP buffer
   const unsigned char* opsrc = OPS_GLOBAL ? static_cast<const unsigned char*>(p.ops) : smem_raw + BARB;
   constexpr bool S3 = S == 3;      // split pipeline: slots A0, A1 = {q, geo}; one B = {flux, residual}
   constexpr size_t AB = QB + GB;
@@ -1131,7 +1358,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   load_codes(0, vc0);
   if (n_it > 1) load_codes(1, vc1);
   issue_tma(0);
-  issue_gather(0, vc0);
+  if constexpr (!GATHER_LATE) issue_gather(0, vc0);
   cp_async_commit();
 
   const int n0 = g * R;
@@ -1150,6 +1377,10 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     if (S3) {
       if (it + 1 < n_it) issue_tma(it + 1);  // into the other {q, geo} buffer (its tile it-1 is done)
       issue_res(it);                         // B's residual: read by this tile's epilogue only
+      if constexpr (GATHER_LATE) {           // this tile's gathers: needed at its flux, after the volume
+        issue_gather(it, vc0);
+        cp_async_commit();
+      }
     }
     if (S == 1 && it + 1 < n_it) prefetch_l2(it + 1);  // its TMA is issued after this tile
     if (S != 1 && it + 2 < n_it) prefetch_l2(it + 2);  // its TMA is issued at the next tile
@@ -1158,9 +1389,11 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     // neighbour gathers go into it; the epilogue then needs this tile's residual
     auto after_lift = [&]() {
       if constexpr (S3) {
-        __syncthreads();
-        if (it + 1 < n_it) issue_gather(it + 1, vc1);
-        cp_async_commit();
+        if constexpr (!GATHER_LATE) {
+          __syncthreads();
+          if (it + 1 < n_it) issue_gather(it + 1, vc1);
+          cp_async_commit();
+        }
         if (RES_TMA && MT::rk && read_res) mbar_wait(bars + 2, (unsigned)(it & 1));
       }
     };
@@ -1168,7 +1401,9 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     const T* sq = sq_of(s);
     const T* gg = sg_of(s) + lane;
     T* sp = sp_of(s);
-    if constexpr (USE_MMA) {
+    if constexpr (DMMA_U) {
+      mma_tile_u<MODE, MAT>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, lane, alpha, read_res, after_lift);
+    } else if constexpr (USE_MMA) {
       if constexpr (DMMA_SPLIT) {
         if (g < PR)
           mma_tile<MODE, MAT, 1>(p, sq, sg_of(s), sp, opsrc, vc0, tile, g, g, lane, alpha, read_res, after_lift);
@@ -1187,13 +1422,23 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
         tf_tile<MODE, MAT, 0>(p, sq, sg_of(s), sp, sr_of(s), opsrc, vc0, tile, g, g, lane, alpha, read_res, after_lift);
       }
     } else {
+    if constexpr (WPRE && MT::vol) {  // W1, W2 of the tile, once (DG_WP)
+      const T* sgs = sg_of(s);
+      for (int i = tid; i < NP * TL; i += TEAM) {
+        const int e = i & (TL - 1);
+        const T hx = sq[i], hy = sq[NP * TL + i];
+        sw[i] = sgs[0 * TL + e] * hy - sgs[2 * TL + e] * hx;
+        sw[NP * TL + i] = sgs[1 * TL + e] * hy - sgs[3 * TL + e] * hx;
+      }
+      if constexpr (!(FLUX_FIRST && MT::surf)) __syncthreads();
+    }
     if constexpr (FLUX_FIRST && MT::surf) {
       flux_points<MAT>(sq, gg, sp, vc0, g, lane, alpha);
       __syncthreads();
     }
     T rhx[R], rhy[R], rez[R];
     if constexpr (MT::vol) {
-      volume_rows(sq, DV, n0, lane, gg[0 * TL], gg[1 * TL], gg[2 * TL], gg[3 * TL], rhx, rhy, rez);
+      volume_rows(sq, DV, n0, lane, gg[0 * TL], gg[1 * TL], gg[2 * TL], gg[3 * TL], rhx, rhy, rez, sw);
     } else if constexpr (MODE == dg::MODE_SURFACE_RK) {
       const T* __restrict__ rv = static_cast<const T*>(p.rhsv);
 #pragma unroll
@@ -1443,7 +1688,7 @@ dg::KernelInfo info() {
   k.residual_tma = RES_TMA ? 1 : 0;
   k.teams_cap = DG_C;
   k.flags = USE_TC ? 0 : (FLUX_FIRST ? 1 : 0) | (OPS_GLOBAL ? 2 : 0) | (FX ? 4 : 0) | (USE_TF && IL ? 8 : 0) |
-                         (ZC_CONN ? 16 : 0) | (ZC && !ZC_CONN ? 32 : 0);
+                         (ZC_CONN ? 16 : 0) | (ZC && !ZC_CONN ? 32 : 0) | (WPRE ? 64 : 0) | (DMMA_U ? 128 : 0);
   return k;
 }
 

@@ -304,7 +304,8 @@ class Context:
                     residual_tma=bool(k.residual_tma), teams_cap=k.teams_cap, smem_bytes=k.smem_bytes,
                     flux_first=bool(k.flags & 1), ops_global=bool(k.flags & 2),
                     flux_in_fragments=bool(k.flags & 4), pass_interleave=bool(k.flags & 8),
-                    compressed_connectivity=bool(k.flags & 16), compressed_geometry=bool(k.flags & 48))
+                    compressed_connectivity=bool(k.flags & 16), compressed_geometry=bool(k.flags & 48),
+                    w_precomputed=bool(k.flags & 64), dmma_units=bool(k.flags & 128))
 
     def kernel_stats(self):
         st = KernelStats()

@@ -45,7 +45,11 @@ def test_kernel_config_matches_tune_table(prec):
         want = ("3xtf32" if prec == 4 else "dmma_fp64") if t["M"] else "fma"
         assert k["contraction"] == want, (N, k)
         assert k["slots"] == t["S"] and k["teams_cap"] == t["C"]
-        assert k["residual_tma"] == bool(t["M"] and prec == 4 and t.get("Q", 1))
+        # residual staged by TMA: the 3xTF32 path (fp32) and the DMMA unit teams (fp64, M=4), knob Q
+        assert k["residual_tma"] == bool(t["M"] in ((1, 2) if prec == 4 else (4,)) and t.get("Q", 1))
+        assert k["dmma_units"] == (prec == 8 and t["M"] == 4)
+        if k["dmma_units"]:
+            assert k["threads"] == 32 * t["U"] and t["U"] % 4 == 0
         assert k["flux_first"] == bool(t.get("F", 0))
         assert k["ops_global"] == bool(t.get("G", 0))
         assert k["flux_in_fragments"] == bool(t["M"] == 1 and prec == 4 and t.get("X", 0))

@@ -64,7 +64,8 @@ def name_of(k):
     return (f"R{k['R']}_S{k['S']}_C{k['C']}_M{k['M']}" + (f"_Q{k['Q']}" if "Q" in k else "")
             + (f"_F{k['F']}" if "F" in k else "") + (f"_G{k['G']}" if "G" in k else "")
             + (f"_X{k['X']}" if "X" in k else "") + (f"_I{k['I']}" if "I" in k else "")
-            + (f"_W{k['W']}" if "W" in k else ""))
+            + (f"_W{k['W']}" if "W" in k else "")
+            + "".join(f"_{x}{k[x]}" for x in ("Z", "U", "L", "Y") if x in k))
 
 
 def cmd_build():
@@ -176,8 +177,7 @@ def cmd_pick(*paths):
         kn.setdefault("X", 0)  # sweeps before the knob existed: flux through shared memory
         kn.setdefault("I", 0)  # sweeps before the knob existed: products accumulator by accumulator
         kn.setdefault("W", 0)  # sweeps before the knob existed: streaming stores
-        tune[key] = dict(R=kn["R"], S=kn["S"], C=kn["C"], M=kn["M"], Q=kn["Q"], F=kn["F"], G=kn["G"],
-                         X=kn["X"], I=kn["I"], W=kn["W"], ms=round(r["ms"], 5))
+        tune[key] = dict(kn, ms=round(r["ms"], 5))  # every knob letter of the variant name (Z, U, L, Y ...)
     out = os.path.join(ROOT, "paper_1304_5546_b200", "csrc", "tune.json")
     with open(out, "w") as fh:
         json.dump(tune, fh, indent=1)
