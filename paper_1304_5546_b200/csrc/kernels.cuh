@@ -77,6 +77,17 @@ constexpr bool DMMA_U = !F32 && DG_MMA == 4;
 #ifndef DG_PU
 #define DG_PU 8
 #endif
+// DG_WS (DMMA_U, fused stage): warp-specialised team -- the PU DMMA warps run volume -> LIFT -> LSERK4
+// epilogue of tile t while WF = 4 flux warps gather the neighbour traces of tile t+1 and form its flux
+// into the other of two flux buffers (mbarrier hand-off), so the flux leaves the DMMA warps' critical path
+#ifndef DG_WS
+#define DG_WS 0
+#endif
+constexpr bool WS = DMMA_U && DG_WS;
+#ifndef DG_WF
+#define DG_WF 4
+#endif
+constexpr int WF = DG_WF;  // flux warps
 // fp32 only: the same contractions as 3xTF32 products on the tensor cores (mma.sync
 // m16n8k8: A = fields, elements x nodes; B = operator^T), split hi + lo so the result
 // keeps fp32 accuracy -- DG_MMA=1: one 16-element m-tile per warp, two warps per tile;
@@ -174,6 +185,15 @@ constexpr size_t SPB = (size_t)3 * NFE * TL * sizeof(T);
 #define DG_RT 1
 #endif
 constexpr bool RES_TMA = (USE_TF || DMMA_U) && DG_RT;
+// DG_TS (3xTF32 path, one slot, residual by TMA): the LSERK4 epilogue writes the new residual and q
+// IN PLACE into the tile's shared-memory residual and field buffers, and one thread streams both tiles
+// out with TMA bulk stores (cp.async.bulk.global.shared::cta) -- 6 bulk copies per tile instead of
+// 72 scattered 4-byte STG per thread; the next tile's TMA load into the slot waits for the stores'
+// shared-memory reads (cp.async.bulk.wait_group.read)
+#ifndef DG_TS
+#define DG_TS 0
+#endif
+constexpr bool TMA_ST = DG_TS != 0;  // (also the warp-specialised DMMA kernel, stage_kernel_ws)
 // DG_FF: phase order of the fused kernels.  0: volume -> flux -> LIFT (the volume
 // accumulators stay live across the flux phase); 1: flux -> volume -> LIFT (nothing but the
 // face-point codes is live during the flux phase, so the peak register count drops)
@@ -196,12 +216,18 @@ __host__ __device__ constexpr size_t slot_bytes(bool surf, bool mat, bool rk) {
 #define DG_WP 0
 #endif
 constexpr bool WPRE = DG_WP && DG_MMA == 0;
-// DG_GL (S = 3 pipeline): a tile's cross-tile neighbour gathers are issued at the tile's own start
-// (after its barrier) and each thread waits for its own cp.async groups right before its flux points
-// (the thread that gathers a point is the thread that forms its flux); with DG_GL = 0 they are issued
-// right after the previous tile's LIFT, where their queued copies hold up that tile's epilogue stores
+// DG_GL: each thread waits for its own cross-tile neighbour gathers (cp.async) right before its flux
+// points -- the thread that gathers a point is the thread that forms its flux -- instead of at the top
+// of the tile, so the gather latency hides behind the volume phase.  With S = 3 the gathers are also
+// ISSUED at the tile's own start (after its barrier) rather than right after the previous tile's LIFT,
+// where their queued copies hold up that tile's epilogue stores
 #ifndef DG_GL
 #define DG_GL 0
+#endif
+// DG_PD: L2 prefetch distance in tiles beyond the next TMA (cp.async.bulk.prefetch.L2 of tile it + PD
+// (S = 1) or it + 1 + PD (S = 2, 3) while tile it computes)
+#ifndef DG_PD
+#define DG_PD 1
 #endif
 constexpr size_t BARB = 64;  // mbarriers: one per slot
 constexpr size_t WPB = WPRE ? (size_t)2 * NP * TL * sizeof(T) : 0;  // DG_WP buffer: W1, W2 [NP][32]
@@ -219,7 +245,10 @@ __host__ __device__ constexpr size_t smem_total(int S, bool surf, bool mat, bool
 #define DG_S (sizeof(DG_T) == 4 ? 1 : 2)
 #endif
 __host__ __device__ constexpr int nslots(bool, bool) { return DG_S; }
-constexpr bool GATHER_LATE = DG_GL && DG_S == 3;
+constexpr bool GATHER_WAIT_LATE = DG_GL;            // each thread waits for its own gathers at its flux
+constexpr bool GATHER_LATE = DG_GL && DG_S == 3;     // S = 3: and issues them at the tile's own start
+static_assert(!TMA_ST || (USE_TF && RES_TMA && DG_S == 1) || (DMMA_U && DG_WS && RES_TMA),
+              "DG_TS: 3xTF32 path with DG_RT = 1 and one slot, or the warp-specialised DMMA kernel with DG_RT = 1");
 constexpr int CTAS_BY_SMEM = (int)((227 * 1024) / smem_total(nslots(true, false), true, false, true));
 #ifndef DG_C
 #define DG_C 5  // measured (C4 fp32): 5 teams x 128 registers beats 8 x 80 (spills) and 4 x 168
@@ -266,7 +295,7 @@ __device__ __forceinline__ void st_out(V* p, const V& v) {
 }
 constexpr int KLT_ = (NF + 7) / 8;
 constexpr int KCODE = FX ? 4 * KLT_ : KPT;  // codes per thread
-static_assert(!(FX && GATHER_LATE), "DG_GL is not implemented with DG_FX");
+static_assert(!(FX && GATHER_WAIT_LATE), "DG_GL is not implemented with DG_FX");
 static_assert(DG_FF != 2 || DMMA_U, "DG_FF = 2 is implemented for the DMMA_U tiles only");
 struct PointElem { int m, e; };
 __device__ __forceinline__ PointElem pair_of(int g, int lane, int k) {  // m = NF: no point
@@ -320,6 +349,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_barrier(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                    smem_u32(dst)),
@@ -327,6 +362,13 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
                : "memory");
 }
 
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -496,7 +538,10 @@ __device__ __forceinline__ void flux_one(const TT* __restrict__ sq, const TT* __
 template <bool MAT>
 __device__ __forceinline__ void flux_points(const T* __restrict__ sq, const T* __restrict__ gg, T* __restrict__ sp,
                                             const int32_t (&vmc)[KCODE], int g, int lane, T alpha) {
-  if constexpr (GATHER_LATE) cp_async_wait_all();  // this thread's own neighbour gathers (DG_GL)
+  if constexpr (GATHER_WAIT_LATE) {  // this thread's own neighbour gathers (DG_GL)
+    if constexpr (DG_S == 2) cp_async_wait_group<1>();  // (the next tile's group may stay in flight)
+    else cp_async_wait_all();
+  }
   T fz[3][3];
   if constexpr (ZC && !MAT) zc_faces(gg, fz);
 #pragma unroll
@@ -856,8 +901,14 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
           const int c = F0 + f;
           TT rs = dt * acc[f][nt][r];
           if (read_res) rs = fma(a, RES_TMA ? sr[c * NP * TL + o] : rr[f][nt][r], rs);
-          if (p.write_res) st_out(res + c * p.vstride + o, rs);
-          st_out(qo + c * p.fstride + o, fma(b, rs, sq[c * NP * TL + o]));
+          const TT qn = fma(b, rs, sq[c * NP * TL + o]);
+          if constexpr (TMA_ST) {  // in place; the bulk stores follow the tile (stage_kernel)
+            const_cast<TT*>(sr)[c * NP * TL + o] = rs;
+            const_cast<TT*>(sq)[c * NP * TL + o] = qn;
+          } else {
+            if (p.write_res) st_out(res + c * p.vstride + o, rs);
+            st_out(qo + c * p.fstride + o, qn);
+          }
         }
       } else {
         TT* __restrict__ out = static_cast<TT*>(p.out) + tbase;
@@ -865,6 +916,7 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
         for (int f = 0; f < NFLD; ++f) out[(F0 + f) * p.vstride + o] = acc[f][nt][r];
       }
     }
+  if constexpr (TMA_ST && MT::rk) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------- phase C: lift
@@ -1037,12 +1089,19 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
 // Per k-step the warp loads the B fragments of its n-tile once (Ez, and W1, W2 formed from Hx, Hy)
 // and issues them against the A fragments (operator rows) of each of its row groups.  Same algebra as
 // mma_tile: u = Dr Ez, v = Ds Ez, w = Dr W1 + Ds W2 -> flux -> rhs += LIFT f -> 1/mu, 1/eps -> LSERK4.
-template <int MODE, bool MAT, typename TT, typename HOOK>
+struct NoHook {
+  __device__ void operator()() const {}
+};
+// WSM (warp-specialised kernel, stage_kernel_ws): the flux is formed by the flux warps -- flux_wait()
+// blocks until this tile's flux is in sp, flux_done() releases sp after the LIFT has read it
+template <int MODE, bool MAT, bool WSM = false, typename TT, typename HOOK, typename FW = NoHook, typename FD = NoHook>
 __device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
                                            TT* __restrict__ sp, const TT* __restrict__ sr,
                                            const unsigned char* __restrict__ ops, const int32_t (&vmc)[KCODE],
-                                           int tile, int g, int lane, TT alpha, bool read_res, const HOOK& after_lift) {
+                                           int tile, int g, int lane, TT alpha, bool read_res, const HOOK& after_lift,
+                                           const FW& flux_wait = FW(), const FD& flux_done = FD()) {
   using MT = ModeTraits<MODE>;
+  static_assert(!WSM || (!FLUX_FIRST && MODE == dg::MODE_FUSED_RK), "warp-specialised tiles: fused stage, volume first");
   using V2 = double2;
   const int nt = g & 3, rg0 = g >> 2;
   auto rg_of = [&](int i) { return rg0 + i * UST; };
@@ -1123,7 +1182,9 @@ __device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __r
     }
   }
   if constexpr (MT::surf) {
-    if constexpr (!FLUX_FIRST) {
+    if constexpr (WSM) {
+      flux_wait();
+    } else if constexpr (!FLUX_FIRST) {
       flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
       __syncthreads();
     } else if constexpr (FLUX_FIRST_NB) {
@@ -1146,6 +1207,7 @@ __device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __r
       }
     }
   }
+  if constexpr (WSM) flux_done();
   after_lift();
   if constexpr (MAT) {
     if (MODE != dg::MODE_VOLUME || p.scale_volume) {
@@ -1183,12 +1245,17 @@ __device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __r
           rs.x = fma(a, ro.x, rs.x);
           rs.y = fma(a, ro.y, rs.y);
         }
-        if (p.write_res) st_out(reinterpret_cast<V2*>(res + c * p.vstride + off), rs);
         const V2 qi = *reinterpret_cast<const V2*>(sq + (c * NP + n) * TL + col);
         V2 qn;
         qn.x = fma(b, rs.x, qi.x);
         qn.y = fma(b, rs.y, qi.y);
-        st_out(reinterpret_cast<V2*>(qo + c * p.fstride + off), qn);
+        if constexpr (WSM && TMA_ST) {  // in place; stage_kernel_ws streams the tile out by TMA
+          *reinterpret_cast<V2*>(const_cast<TT*>(sr) + (c * NP + n) * TL + col) = rs;
+          *reinterpret_cast<V2*>(const_cast<TT*>(sq) + (c * NP + n) * TL + col) = qn;
+        } else {
+          if (p.write_res) st_out(reinterpret_cast<V2*>(res + c * p.vstride + off), rs);
+          st_out(reinterpret_cast<V2*>(qo + c * p.fstride + off), qn);
+        }
       }
     } else {
       TT* __restrict__ out = static_cast<TT*>(p.out);
@@ -1201,6 +1268,7 @@ __device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __r
       }
     }
   }
+  if constexpr (WSM && TMA_ST) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 // Persistent, software-pipelined stage kernel (one team per CTA).
@@ -1358,6 +1426,8 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   load_codes(0, vc0);
   if (n_it > 1) load_codes(1, vc1);
   issue_tma(0);
+#pragma unroll 1
+  for (int d = (S == 1 ? 1 : 2); d < (S == 1 ? 0 : 1) + DG_PD && d < n_it; ++d) prefetch_l2(d);  // DG_PD > 1
   if constexpr (!GATHER_LATE) issue_gather(0, vc0);
   cp_async_commit();
 
@@ -1365,7 +1435,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   const T alpha = static_cast<T>(p.alpha);
   for (int it = 0; it < n_it; ++it) {
     const int s = slot_of_it(it);
-    cp_async_wait_all();                                                   // gathers of tile it
+    if constexpr (!GATHER_WAIT_LATE) cp_async_wait_all();                  // gathers of tile it
     mbar_wait(bars + s, (unsigned)(S3 ? (it >> 1) & 1 : (it / S) & 1));  // TMA: fields + geometry of tile it
     __syncthreads();
     const int tile = tile_of(it);
@@ -1382,8 +1452,9 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
         cp_async_commit();
       }
     }
-    if (S == 1 && it + 1 < n_it) prefetch_l2(it + 1);  // its TMA is issued after this tile
-    if (S != 1 && it + 2 < n_it) prefetch_l2(it + 2);  // its TMA is issued at the next tile
+    // L2 prefetch distance: S = 1 issues tile it+1's TMA after this tile, S = 2/3 at the next tile
+    constexpr int PFD = (S == 1 ? 0 : 1) + DG_PD;
+    if (it + PFD < n_it) prefetch_l2(it + PFD);
     if (it + 2 < n_it) load_codes(it + 2, vc2);
     // after the LIFT (S = 3): every warp is done with the flux buffer -> the next tile's
     // neighbour gathers go into it; the epilogue then needs this tile's residual
@@ -1514,14 +1585,208 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       }
     }
     }  // !USE_MMA
-    if (S == 1 && it + 1 < n_it) {
+    if constexpr (TMA_ST && MT::rk) {  // the tile's new residual and fields, from shared memory (DG_TS)
       __syncthreads();
+      if (tid == 0) {
+        const int64_t t0 = (int64_t)tile * NP * TL;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (p.write_res) tma_store_1d(static_cast<T*>(p.res) + c * p.vstride + t0, sr_of(s) + c * NP * TL, (unsigned)(QB / 3));
+          tma_store_1d(static_cast<T*>(p.q_out) + c * p.fstride + t0, sq_of(s) + c * NP * TL, (unsigned)(QB / 3));
+        }
+        bulk_commit();
+      }
+    }
+    if (S == 1 && it + 1 < n_it) {
+      if constexpr (!(TMA_ST && MT::rk)) __syncthreads();
+      if (TMA_ST && MT::rk && tid == 0) bulk_wait_read();  // the slot's bulk stores have read it
       issue_tma(it + 1);
       issue_gather(it + 1, vc1);
       cp_async_commit();
     }
 #pragma unroll
     for (int k = 0; k < KCODE; ++k) { vc0[k] = vc1[k]; vc1[k] = vc2[k]; }
+  }
+  if (TMA_ST && MT::rk && tid == 0) bulk_wait_all();  // shared memory stays valid until the stores are done
+}
+
+
+// ---------------------------------------------------------------- warp-specialised fused stage (DG_WS)
+// Shared memory: mbarriers | operators | A0, A1 = {q, geo} (tile t in A[t & 1], TMA) | F0, F1 flux
+// buffers | the residual buffer (RES_TMA).  mbarriers: 0, 1 A loaded (tx); 2 residual loaded (tx);
+// 3, 4 flux of F[b] formed (WF x 32 arrivals); 5, 6 F[b] read by the LIFT (TEAM_M arrivals).
+// DMMA warps (0 .. PU-1), tile t, b = t & 1:  wait A[b] -> (thread 0: residual TMA) -> volume ->
+//   wait flux[b] -> LIFT -> release F[b] -> wait residual -> epilogue -> named barrier -> (thread 0: TMA of
+//   tile t+2 into A[b]; its L2 prefetch of tile t+3)
+// flux warps (PU .. PU+3), tile t:  wait A[b] -> wait F[b] released by the LIFT of tile t-2 -> cp.async
+//   gathers of the cross-tile neighbour traces into F[b] -> wait own copies -> flux -> arrive flux[b].
+// A[b] is free once the DMMA warps' epilogue of tile t is done: their LIFT waited for the flux warps'
+// flux of tile t, the flux warps' last use of A[b].
+constexpr int TEAM_M = P * 32;
+constexpr int TEAM_WS = TEAM_M + WF * 32;
+constexpr int KF = (NF + WF - 1) / WF;  // face points per flux thread: m = gf + k WF, element = lane
+static_assert(!(WS && ZC_CONN), "DG_WS reads per-point neighbour codes (not with DG_ZC = 1)");
+__host__ __device__ constexpr size_t ws_smem(bool mat) {
+  return BARB + OPB_SMEM + 2 * (QB + geo_bytes(mat)) + 2 * SPB + (RES_TMA ? QB : 0);
+}
+template <int MODE, bool MAT>
+__global__ void __launch_bounds__(TEAM_WS, 1) stage_kernel_ws(const dg::StageArgs p) {
+  static_assert(MODE == dg::MODE_FUSED_RK, "the warp-specialised kernel runs the fused stage");
+  constexpr int NG = ngeo(MAT);
+  constexpr size_t GB = geo_bytes(MAT);
+  constexpr size_t AB = QB + GB;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const T* __restrict__ q = static_cast<const T*>(p.q_in);
+  const T* __restrict__ geo = static_cast<const T*>(p.geo);
+  const int tid = threadIdx.x, g = tid >> 5, lane = tid & 31;
+  const int first = blockIdx.x, stride = gridDim.x;
+  const int n_it = first < p.ntiles ? (p.ntiles - first + stride - 1) / stride : 0;
+  if (n_it == 0) return;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  unsigned char* abuf = smem_raw + BARB + OPB_SMEM;
+  auto sq_of = [&](int b) { return reinterpret_cast<T*>(abuf + b * AB); };
+  auto sg_of = [&](int b) { return reinterpret_cast<T*>(abuf + b * AB + QB); };
+  auto sp_of = [&](int b) { return reinterpret_cast<T*>(abuf + 2 * AB + b * SPB); };
+  T* const sr = reinterpret_cast<T*>(abuf + 2 * AB + 2 * SPB);
+  const bool read_res = p.a != 0.0;
+  auto tile_of = [&](int it) {
+    const int sidx = first + it * stride;
+    const int j = p.reverse ? p.ntiles - 1 - sidx : sidx;
+    return p.tiles ? p.tiles[j] : j;
+  };
+  auto issue_tma = [&](int it) {  // fields + geometry of tile it into A[it & 1]
+    const int tile = tile_of(it), b = it & 1;
+    mbar_expect_tx(bars + b, (unsigned)AB);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      tma_load_1d(sq_of(b) + c * NP * TL, q + c * p.fstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bars + b);
+    tma_load_1d(sg_of(b), geo + (int64_t)tile * NG * TL, (unsigned)GB, bars + b);
+  };
+  auto prefetch_l2 = [&](int it) {
+    const int tile = tile_of(it);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) bulk_prefetch_l2(q + c * p.fstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3));
+    bulk_prefetch_l2(geo + (int64_t)tile * NG * TL, (unsigned)GB);
+    if (RES_TMA && read_res) {
+      const T* res = static_cast<const T*>(p.res);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) bulk_prefetch_l2(res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3));
+    }
+  };
+  // prologue: barriers, operators, the first two tiles
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) mbar_init(bars + b, 1);
+    mbar_init(bars + 2, 1);
+    for (int b = 0; b < 2; ++b) mbar_init(bars + 3 + b, WF * 32);
+    for (int b = 0; b < 2; ++b) mbar_init(bars + 5 + b, TEAM_M);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  {
+    const int4* src = reinterpret_cast<const int4*>(p.ops);
+    int4* dst = reinterpret_cast<int4*>(smem_raw + BARB);
+    for (int i = tid; i < (int)(OPB_SMEM / 16); i += TEAM_WS) cp_async16(dst + i, src + i);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  if (tid == 0) {
+    issue_tma(0);
+    if (n_it > 1) issue_tma(1);
+    if (n_it > 2) prefetch_l2(2);
+  }
+  const T alpha = static_cast<T>(p.alpha);
+  if (g < P) {  // ------------------------------------------------------------- DMMA warps
+    const int32_t nocodes[KCODE] = {};
+    for (int it = 0; it < n_it; ++it) {
+      const int b = it & 1;
+      const int tile = tile_of(it);
+      if (TMA_ST && tid == 0 && it >= 1) {  // tile it-1's bulk stores have read A[b ^ 1] and sr
+        bulk_wait_read();
+        if (it + 1 < n_it) issue_tma(it + 1);
+      }
+      mbar_wait(bars + b, (unsigned)((it >> 1) & 1));
+      if (RES_TMA && read_res && tid == 0) {  // sr is free: the previous epilogue ended at the named barrier
+        mbar_expect_tx(bars + 2, (unsigned)QB);
+        const T* res = static_cast<const T*>(p.res);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          tma_load_1d(sr + c * NP * TL, res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bars + 2);
+      }
+      auto flux_wait = [&]() { mbar_wait(bars + 3 + b, (unsigned)((it >> 1) & 1)); };
+      auto flux_done = [&]() { mbar_arrive(bars + 5 + b); };
+      auto after_lift = [&]() {
+        if (RES_TMA && read_res) mbar_wait(bars + 2, (unsigned)(it & 1));
+        if constexpr (TMA_ST) named_barrier(1, TEAM_M);  // no DMMA warp still reads A[b] in its volume
+      };
+      mma_tile_u<MODE, MAT, true>(p, sq_of(b), sg_of(b), sp_of(b), sr, smem_raw + BARB, nocodes, tile, g, lane,
+                                  alpha, read_res, after_lift, flux_wait, flux_done);
+      named_barrier(1, TEAM_M);  // every DMMA warp is done with A[b] and sr
+      if (tid == 0) {
+        if constexpr (TMA_ST) {  // the new q and residual of the tile, written in place (DG_TS)
+          const int64_t t0 = (int64_t)tile * NP * TL;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (p.write_res) tma_store_1d(static_cast<T*>(p.res) + c * p.vstride + t0, sr + c * NP * TL, (unsigned)(QB / 3));
+            tma_store_1d(static_cast<T*>(p.q_out) + c * p.fstride + t0, sq_of(b) + c * NP * TL, (unsigned)(QB / 3));
+          }
+          bulk_commit();
+        } else {
+          if (it + 2 < n_it) issue_tma(it + 2);
+        }
+        if (it + 3 < n_it) prefetch_l2(it + 3);
+      }
+    }
+    if (TMA_ST && tid == 0) bulk_wait_all();
+  } else {  // ------------------------------------------------------------------ flux warps
+    const int gf = g - P;
+    int32_t cc[KF], cn[KF];  // neighbour codes of tiles it, it+1
+    auto load_codes = [&](int it, int32_t (&v)[KF]) {
+      const int32_t* src = p.vmapP + (int64_t)tile_of(it) * NF * TL;
+#pragma unroll
+      for (int k = 0; k < KF; ++k) {
+        const int m = gf + k * WF;
+        v[k] = m < NF ? __ldg(src + m * TL + lane) : -1;
+      }
+    };
+    load_codes(0, cc);
+    for (int it = 0; it < n_it; ++it) {
+      const int b = it & 1;
+      if (it + 1 < n_it) load_codes(it + 1, cn);
+      if (it >= 2) mbar_wait(bars + 5 + b, (unsigned)(((it >> 1) + 1) & 1));  // F[b]: LIFT of tile it-2 done
+      T* sp = sp_of(b);
+#pragma unroll
+      for (int k = 0; k < KF; ++k) {  // cross-tile neighbour traces (same-tile ones: from A[b])
+        const int m = gf + k * WF;
+        if (m < NF && cc[k] >= 0) {
+          const T* src = q + cc[k];
+          T* dst = sp + m * TL + colx(m, lane);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) cp_async_small<sizeof(T)>(dst + c * NFE * TL, src + c * p.fstride);
+        }
+      }
+      cp_async_commit();
+      mbar_wait(bars + b, (unsigned)((it >> 1) & 1));  // A[b]: own traces, same-tile neighbours, geometry
+      cp_async_wait_all();
+      const T* sq = sq_of(b);
+      const T* gg = sg_of(b) + lane;
+      T fz[3][3];
+      if constexpr (ZC && !MAT) zc_faces(gg, fz);
+#pragma unroll
+      for (int k = 0; k < KF; ++k) {
+        const int m = gf + k * WF;
+        if (m >= NF) break;
+        const int f = m / NFP;
+        T fHx, fHy, fEz;
+        flux_one<MAT>(sq, gg, sp, cc[k], m, f, lane, alpha, fHx, fHy, fEz, fz);
+        const int pm = m * TL + colx(m, lane);
+        sp[0 * NFE * TL + pm] = fHx;
+        sp[1 * NFE * TL + pm] = fHy;
+        sp[2 * NFE * TL + pm] = fEz;
+      }
+      mbar_arrive(bars + 3 + b);  // release: the flux of tile it is in F[b]
+#pragma unroll
+      for (int k = 0; k < KF; ++k) cc[k] = cn[k];
+    }
   }
 }
 
@@ -1533,6 +1798,29 @@ cudaError_t launch_one(const dg::StageArgs& a, cudaStream_t s) {
     return tc::launch_one<MODE, MAT>(a, s);
   } else {
   using MT = ModeTraits<MODE>;
+  if constexpr (WS && MODE == dg::MODE_FUSED_RK) {  // warp-specialised fused stage: one CTA per SM
+    constexpr size_t smem = ws_smem(MAT);
+    static int grid_ws[64] = {0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 64) return cudaErrorInvalidDevice;
+    if (grid_ws[dev] == 0) {
+      e = cudaFuncSetAttribute(stage_kernel_ws<MODE, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return cudaGetLastError(), e;
+      int per_sm = 0, sms = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_kernel_ws<MODE, MAT>, TEAM_WS, smem);
+      if (e != cudaSuccess) return e;
+      e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (e != cudaSuccess) return e;
+      grid_ws[dev] = (per_sm > 0 ? per_sm : 1) * sms;
+    }
+    int grid = a.ntiles < grid_ws[dev] ? a.ntiles : grid_ws[dev];
+    if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
+    if (grid <= 0) return cudaSuccess;
+    stage_kernel_ws<MODE, MAT><<<grid, TEAM_WS, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   constexpr size_t smem = smem_total(nslots(MT::surf, MAT), MT::surf, MAT, MT::rk);
   static int grid_cap[64] = {0};  // resident CTAs (whole GPU) per device ordinal
   int dev = 0;
@@ -1679,16 +1967,16 @@ dg::KernelInfo info() {
   dg::KernelInfo k;
   k.N = N;
   k.prec = (int)sizeof(T);
-  k.threads = USE_TC ? tc::NTH : TEAM;
+  k.threads = USE_TC ? tc::NTH : (WS ? TEAM_WS : TEAM);
   k.slots = USE_TC ? 1 : nslots(true, false);
   k.row_groups = P;
   k.rows_per_group = R;
-  k.smem_bytes = USE_TC ? tc::smem_bytes(false) : smem_total(nslots(true, false), true, false, true);
+  k.smem_bytes = USE_TC ? tc::smem_bytes(false) : (WS ? ws_smem(false) : smem_total(nslots(true, false), true, false, true));
   k.contraction = USE_TC ? 3 : (USE_TF ? 2 : (USE_MMA ? 1 : 0));
   k.residual_tma = RES_TMA ? 1 : 0;
   k.teams_cap = DG_C;
   k.flags = USE_TC ? 0 : (FLUX_FIRST ? 1 : 0) | (OPS_GLOBAL ? 2 : 0) | (FX ? 4 : 0) | (USE_TF && IL ? 8 : 0) |
-                         (ZC_CONN ? 16 : 0) | (ZC && !ZC_CONN ? 32 : 0) | (WPRE ? 64 : 0) | (DMMA_U ? 128 : 0);
+                         (ZC_CONN ? 16 : 0) | (ZC && !ZC_CONN ? 32 : 0) | (WPRE ? 64 : 0) | (DMMA_U ? 128 : 0) | (WS ? 256 : 0);
   return k;
 }
 

@@ -305,7 +305,8 @@ class Context:
                     flux_first=bool(k.flags & 1), ops_global=bool(k.flags & 2),
                     flux_in_fragments=bool(k.flags & 4), pass_interleave=bool(k.flags & 8),
                     compressed_connectivity=bool(k.flags & 16), compressed_geometry=bool(k.flags & 48),
-                    w_precomputed=bool(k.flags & 64), dmma_units=bool(k.flags & 128))
+                    w_precomputed=bool(k.flags & 64), dmma_units=bool(k.flags & 128),
+                    warp_specialised=bool(k.flags & 256))
 
     def kernel_stats(self):
         st = KernelStats()

@@ -113,6 +113,31 @@ def test_grid_and_tile_order_never_change_the_result(N, prec):
                 assert np.array_equal(a, b), (max_ctas, order)
 
 
+@pytest.mark.parametrize("N", [5, 6, 7, 8])
+def test_fp64_dmma_teams_partitions_bitwise(N):
+    """The fp64 DMMA unit teams (N >= 5) and the warp-specialised kernel (DMMA warps + flux warps,
+    N = 6-8): 3 in-process partitions -- the NCCL path's interior-then-boundary tile lists, halo by
+    device copies -- give bitwise the fields of one partition (P17), as do grid caps and tile order."""
+    VX, VY, E, eps, mu, q0, dt, _ = _case(N, False)
+    c = dg.dg_setup(N, VX, VY, E, precision=8)
+    cfg = c.kernel_config()
+    c.set_fields(*q0)
+    c.run(dt, 7)
+    ref = c.get_fields()
+    c.destroy()
+    assert cfg["dmma_units"], cfg
+    cs = [dg.dg_setup(N, VX, VY, E, precision=8, rank=r, nranks=3, transport=1, max_ctas=2, tile_order=1)
+          for r in range(3)]
+    for c in cs:
+        c.set_fields(*(a[c.local_elements()] for a in q0))
+    dg.dg_run_group(cs, dt, 7)
+    for c in cs:
+        gid = c.local_elements()
+        for a, b in zip(c.get_fields(), ref):
+            assert np.array_equal(a, b[gid])
+        c.destroy()
+
+
 def test_check_every_reports_first_bad_step():
     VX, VY, E = dginputs.rect_mesh(4)
     for every, want in ((1, 1), (3, 3)):

@@ -48,8 +48,10 @@ def test_kernel_config_matches_tune_table(prec):
         # residual staged by TMA: the 3xTF32 path (fp32) and the DMMA unit teams (fp64, M=4), knob Q
         assert k["residual_tma"] == bool(t["M"] in ((1, 2) if prec == 4 else (4,)) and t.get("Q", 1))
         assert k["dmma_units"] == (prec == 8 and t["M"] == 4)
-        if k["dmma_units"]:
-            assert k["threads"] == 32 * t["U"] and t["U"] % 4 == 0
+        assert k["warp_specialised"] == (prec == 8 and t["M"] == 4 and bool(t.get("K", 0)))
+        if k["dmma_units"]:  # U DMMA warps (a multiple of 4), plus H flux warps when warp-specialised
+            assert t["U"] % 4 == 0
+            assert k["threads"] == 32 * (t["U"] + (t.get("H", 4) if t.get("K", 0) else 0))
         assert k["flux_first"] == bool(t.get("F", 0))
         assert k["ops_global"] == bool(t.get("G", 0))
         assert k["flux_in_fragments"] == bool(t["M"] == 1 and prec == 4 and t.get("X", 0))

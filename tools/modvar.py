@@ -47,9 +47,9 @@ def build(tag, specs):
         lines = (p.stdout + p.stderr).splitlines()
         regs = []
         for i, ln in enumerate(lines):  # the fused kernels: stage_kernel<0, false/true>
-            if "Compiling entry function" in ln and "stage_kernelILi0ELb" in ln:
+            if "Compiling entry function" in ln and ("stage_kernelILi0ELb" in ln or "stage_kernel_wsILi0ELb" in ln):
                 info = " ".join(x.split(":", 1)[-1].strip() for x in lines[i + 1:i + 4] if "spill" in x or "registers" in x)
-                regs.append(("mat " if "ILi0ELb1" in ln else "const ") + info)
+                regs.append(("ws " if "_ws" in ln else "") + ("mat " if "ILi0ELb1" in ln else "const ") + info)
         objs = [obj if o.endswith(f"k_{tag}.o") else o for o in main_objs]
         lib = os.path.join(vdir, f"{name}.so")
         B.run([B.NVCC, "-shared", "-o", lib] + objs + B.ARCH + ["-ldl"])

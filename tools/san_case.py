@@ -1,7 +1,9 @@
 """Small runs of every stage-kernel family for compute-sanitizer (tools/sanitize.sh): C1 (N=4 fp64),
 the multi-tile persistent pipeline (grid capped: each CTA walks several tiles) for the S=1 fp32
-3xTF32 (N=5), S=3 fp32 FMA (N=3), S=3 fp64 FMA (N=8) and DMMA (N=9) kernels, fused and split, the
-tcgen05 variant (N=5), a two-layer material case, and a 3-partition group run (tile lists + halo)."""
+3xTF32 (N=5), S=3 fp32 FMA (N=3), the fp64 DMMA unit teams (N=5 S=1, N=9 S=3) and warp-specialised
+kernels (N=6, 7, 8: DMMA warps + flux warps, mbarrier hand-offs), fused and split, the tcgen05 variant
+(N=5), a two-layer material case, and 3-partition group runs (tile lists + halo; N=5 and the
+warp-specialised N=8)."""
 import os
 import sys
 
@@ -32,10 +34,13 @@ for fused in (True, False):
     run(5, 4, fused=fused, max_ctas=2)                      # 3xTF32 S=1, 4 tiles per CTA
     run(3, 4, fused=fused, max_ctas=2)                      # FMA S=3 split pipeline
     run(8, 8, fused=fused, max_ctas=2)                      # FMA fp64 S=3
-    run(9, 8, fused=fused, max_ctas=2)                      # DMMA S=3
+    run(9, 8, fused=fused, max_ctas=2)                      # DMMA units S=3
+    run(7, 8, fused=fused, max_ctas=2)                      # warp-specialised DMMA (fused), S=3 (split)
+    run(5, 8, fused=fused, max_ctas=2)                      # DMMA units S=1
 run(5, 4, n=12, max_ctas=1, kernel_variant=1)               # tcgen05, 3 groups per CTA
 run(5, 4, n=12, max_ctas=1, kernel_variant=1, fused=False)
-run(8, 8, material=True, max_ctas=2)
+run(8, 8, material=True, max_ctas=2)                        # warp-specialised, material flux
+run(6, 8, n=12, max_ctas=1)                                 # warp-specialised, one CTA walks every tile
 VX, VY, E = dginputs.jittered_mesh(10, seed=3)
 cs = [dg.dg_setup(5, VX, VY, E, precision=8, rank=r, nranks=3, transport=1, max_ctas=2) for r in range(3)]
 for c in cs:
@@ -46,3 +51,12 @@ for c in cs:
     c.sync()
     c.destroy()
 print("group ok")
+cs = [dg.dg_setup(8, VX, VY, E, precision=8, rank=r, nranks=3, transport=1, max_ctas=2) for r in range(3)]
+for c in cs:
+    x, y = c.nodes()
+    c.set_fields(*dginputs.cavity_mode(x, y, 0.1))
+dg.dg_run_group(cs, 1e-4, 3)
+for c in cs:
+    c.sync()
+    c.destroy()
+print("group ws ok")
