@@ -84,6 +84,10 @@ constexpr bool DMMA_U = !F32 && DG_MMA == 4;
 #define DG_WS 0
 #endif
 constexpr bool WS = DMMA_U && DG_WS;
+// DG_WS = 2: the helper warps also run the LSERK4 epilogue of the previous tile (the DMMA warps hand the
+// rhs over in a shared-memory buffer and release the tile's fields right after the LIFT: the epilogue
+// reads q_in and the residual from global memory / L2)
+constexpr bool WS2 = WS && DG_WS == 2;
 #ifndef DG_WF
 #define DG_WF 4
 #endif
@@ -194,6 +198,9 @@ constexpr bool RES_TMA = (USE_TF || DMMA_U) && DG_RT;
 #define DG_TS 0
 #endif
 constexpr bool TMA_ST = DG_TS != 0;  // (also the warp-specialised DMMA kernel, stage_kernel_ws)
+// DG_TS = 2 (3xTF32 path): the same in-place epilogue, but the tile is then written out by all threads
+// with coalesced 16-byte streaming stores (after a barrier) instead of TMA bulk stores
+constexpr bool SMEM_ST = DG_TS == 2;
 // DG_FF: phase order of the fused kernels.  0: volume -> flux -> LIFT (the volume
 // accumulators stay live across the flux phase); 1: flux -> volume -> LIFT (nothing but the
 // face-point codes is live during the flux phase, so the peak register count drops)
@@ -916,7 +923,7 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
         for (int f = 0; f < NFLD; ++f) out[(F0 + f) * p.vstride + o] = acc[f][nt][r];
       }
     }
-  if constexpr (TMA_ST && MT::rk) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if constexpr (TMA_ST && !SMEM_ST && MT::rk) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------- phase C: lift
@@ -1094,12 +1101,17 @@ struct NoHook {
 };
 // WSM (warp-specialised kernel, stage_kernel_ws): the flux is formed by the flux warps -- flux_wait()
 // blocks until this tile's flux is in sp, flux_done() releases sp after the LIFT has read it
-template <int MODE, bool MAT, bool WSM = false, typename TT, typename HOOK, typename FW = NoHook, typename FD = NoHook>
+// WSE (DG_WS = 2): the LSERK4 epilogue runs in the helper warps -- after the LIFT and the material
+// scaling this tile's rhs goes to the shared-memory accumulator buffer sacc ([3][NP][32], the tile
+// layout) instead of through the update
+template <int MODE, bool MAT, bool WSM = false, bool WSE = false, typename TT, typename HOOK, typename FW = NoHook,
+          typename FD = NoHook>
 __device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
                                            TT* __restrict__ sp, const TT* __restrict__ sr,
                                            const unsigned char* __restrict__ ops, const int32_t (&vmc)[KCODE],
                                            int tile, int g, int lane, TT alpha, bool read_res, const HOOK& after_lift,
-                                           const FW& flux_wait = FW(), const FD& flux_done = FD()) {
+                                           const FW& flux_wait = FW(), const FD& flux_done = FD(),
+                                           TT* __restrict__ sacc = nullptr) {
   using MT = ModeTraits<MODE>;
   static_assert(!WSM || (!FLUX_FIRST && MODE == dg::MODE_FUSED_RK), "warp-specialised tiles: fused stage, volume first");
   using V2 = double2;
@@ -1168,7 +1180,7 @@ __device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __r
       for (int h = 0; h < 2; ++h) rhx[i][h] = rhy[i][h] = rez[i][h] = TT(0);
   }
   V2 rr[UW][3];  // LSERK4 residual pairs (in flight during the surface phase; RES_TMA: staged in sr)
-  if constexpr (MT::rk && !RES_TMA) {
+  if constexpr (MT::rk && !RES_TMA && !WSE) {
     if (read_res) {
       const TT* __restrict__ res = static_cast<const TT*>(p.res);
 #pragma unroll
@@ -1208,7 +1220,7 @@ __device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __r
     }
   }
   if constexpr (WSM) flux_done();
-  after_lift();
+  if constexpr (!WSE) after_lift();
   if constexpr (MAT) {
     if (MODE != dg::MODE_VOLUME || p.scale_volume) {
 #pragma unroll
@@ -1222,6 +1234,25 @@ __device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __r
         }
       }
     }
+  }
+  if constexpr (WSE) {  // rhs -> sacc (after_lift: the tile's buffers are released, sacc is free)
+    after_lift();
+#pragma unroll
+    for (int i = 0; i < UW; ++i) {
+      if (!unit_ok(i)) continue;
+      const int n = 8 * rg_of(i) + (lane >> 2);
+      if (n >= NP) continue;
+      const int col = colx(n, ec0);
+      const TT r3[3][2] = {{rhx[i][0], rhx[i][1]}, {rhy[i][0], rhy[i][1]}, {rez[i][0], rez[i][1]}};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        V2 o;
+        o.x = r3[c][0];
+        o.y = r3[c][1];
+        *reinterpret_cast<V2*>(sacc + (c * NP + n) * TL + col) = o;
+      }
+    }
+    return;
   }
 #pragma unroll
   for (int i = 0; i < UW; ++i) {
@@ -1585,7 +1616,22 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       }
     }
     }  // !USE_MMA
-    if constexpr (TMA_ST && MT::rk) {  // the tile's new residual and fields, from shared memory (DG_TS)
+    if constexpr (SMEM_ST && MT::rk) {  // the tile's new residual and fields, coalesced (DG_TS = 2)
+      __syncthreads();
+      using V4 = typename std::conditional<F32, float4, double2>::type;
+      constexpr int PER = 16 / (int)sizeof(T);
+      const int64_t t0 = (int64_t)tile * NP * TL;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int o = PER * tid; o < NP * TL; o += PER * TEAM) {
+          if (p.write_res)
+            __stcs(reinterpret_cast<V4*>(static_cast<T*>(p.res) + c * p.vstride + t0 + o),
+                   *reinterpret_cast<const V4*>(sr_of(s) + c * NP * TL + o));
+          __stcs(reinterpret_cast<V4*>(static_cast<T*>(p.q_out) + c * p.fstride + t0 + o),
+                 *reinterpret_cast<const V4*>(sq_of(s) + c * NP * TL + o));
+        }
+    } else if constexpr (TMA_ST && MT::rk) {  // the tile's new residual and fields, from shared memory (DG_TS)
       __syncthreads();
       if (tid == 0) {
         const int64_t t0 = (int64_t)tile * NP * TL;
@@ -1599,7 +1645,8 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     }
     if (S == 1 && it + 1 < n_it) {
       if constexpr (!(TMA_ST && MT::rk)) __syncthreads();
-      if (TMA_ST && MT::rk && tid == 0) bulk_wait_read();  // the slot's bulk stores have read it
+      if (SMEM_ST && MT::rk) __syncthreads();                 // every thread's stores have read the slot
+      if (TMA_ST && !SMEM_ST && MT::rk && tid == 0) bulk_wait_read();  // the slot's bulk stores have read it
       issue_tma(it + 1);
       issue_gather(it + 1, vc1);
       cp_async_commit();
@@ -1607,7 +1654,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
 #pragma unroll
     for (int k = 0; k < KCODE; ++k) { vc0[k] = vc1[k]; vc1[k] = vc2[k]; }
   }
-  if (TMA_ST && MT::rk && tid == 0) bulk_wait_all();  // shared memory stays valid until the stores are done
+  if (TMA_ST && !SMEM_ST && MT::rk && tid == 0) bulk_wait_all();  // smem stays valid until the stores are done
 }
 
 
@@ -1622,13 +1669,15 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
 //   gathers of the cross-tile neighbour traces into F[b] -> wait own copies -> flux -> arrive flux[b].
 // A[b] is free once the DMMA warps' epilogue of tile t is done: their LIFT waited for the flux warps'
 // flux of tile t, the flux warps' last use of A[b].
+constexpr size_t BARW = 128;  // the warp-specialised kernel's 9 mbarriers
 constexpr int TEAM_M = P * 32;
 constexpr int TEAM_WS = TEAM_M + WF * 32;
 constexpr int KF = (NF + WF - 1) / WF;  // face points per flux thread: m = gf + k WF, element = lane
 static_assert(!(WS && ZC_CONN), "DG_WS reads per-point neighbour codes (not with DG_ZC = 1)");
 __host__ __device__ constexpr size_t ws_smem(bool mat) {
-  return BARB + OPB_SMEM + 2 * (QB + geo_bytes(mat)) + 2 * SPB + (RES_TMA ? QB : 0);
+  return BARW + OPB_SMEM + 2 * (QB + geo_bytes(mat)) + 2 * SPB + (RES_TMA || WS2 ? QB : 0);
 }
+static_assert(!(WS2 && RES_TMA), "DG_WS = 2 reads the residual in the helper warps (DG_RT = 0)");
 template <int MODE, bool MAT>
 __global__ void __launch_bounds__(TEAM_WS, 1) stage_kernel_ws(const dg::StageArgs p) {
   static_assert(MODE == dg::MODE_FUSED_RK, "the warp-specialised kernel runs the fused stage");
@@ -1643,7 +1692,7 @@ __global__ void __launch_bounds__(TEAM_WS, 1) stage_kernel_ws(const dg::StageArg
   const int n_it = first < p.ntiles ? (p.ntiles - first + stride - 1) / stride : 0;
   if (n_it == 0) return;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
-  unsigned char* abuf = smem_raw + BARB + OPB_SMEM;
+  unsigned char* abuf = smem_raw + BARW + OPB_SMEM;
   auto sq_of = [&](int b) { return reinterpret_cast<T*>(abuf + b * AB); };
   auto sg_of = [&](int b) { return reinterpret_cast<T*>(abuf + b * AB + QB); };
   auto sp_of = [&](int b) { return reinterpret_cast<T*>(abuf + 2 * AB + b * SPB); };
@@ -1667,23 +1716,26 @@ __global__ void __launch_bounds__(TEAM_WS, 1) stage_kernel_ws(const dg::StageArg
 #pragma unroll
     for (int c = 0; c < 3; ++c) bulk_prefetch_l2(q + c * p.fstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3));
     bulk_prefetch_l2(geo + (int64_t)tile * NG * TL, (unsigned)GB);
-    if (RES_TMA && read_res) {
+    if ((RES_TMA || WS2) && read_res) {
       const T* res = static_cast<const T*>(p.res);
 #pragma unroll
       for (int c = 0; c < 3; ++c) bulk_prefetch_l2(res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3));
     }
   };
+  T* const sacc = sr;  // WS2: the rhs hand-over buffer (in place of the residual buffer)
   // prologue: barriers, operators, the first two tiles
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) mbar_init(bars + b, 1);
     mbar_init(bars + 2, 1);
+    mbar_init(bars + 7, TEAM_M);  // WS2: rhs of the tile in sacc (DMMA warps arrive)
+    mbar_init(bars + 8, WF * 32);  // WS2: sacc consumed by the epilogue (helper warps arrive)
     for (int b = 0; b < 2; ++b) mbar_init(bars + 3 + b, WF * 32);
     for (int b = 0; b < 2; ++b) mbar_init(bars + 5 + b, TEAM_M);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   {
     const int4* src = reinterpret_cast<const int4*>(p.ops);
-    int4* dst = reinterpret_cast<int4*>(smem_raw + BARB);
+    int4* dst = reinterpret_cast<int4*>(smem_raw + BARW);
     for (int i = tid; i < (int)(OPB_SMEM / 16); i += TEAM_WS) cp_async16(dst + i, src + i);
   }
   cp_async_commit();
@@ -1718,7 +1770,22 @@ __global__ void __launch_bounds__(TEAM_WS, 1) stage_kernel_ws(const dg::StageArg
         if (RES_TMA && read_res) mbar_wait(bars + 2, (unsigned)(it & 1));
         if constexpr (TMA_ST) named_barrier(1, TEAM_M);  // no DMMA warp still reads A[b] in its volume
       };
-      mma_tile_u<MODE, MAT, true>(p, sq_of(b), sg_of(b), sp_of(b), sr, smem_raw + BARB, nocodes, tile, g, lane,
+      if constexpr (WS2) {
+        // after the LIFT: every DMMA warp is done with A[b] -> TMA of tile it+2; then wait for sacc
+        auto release = [&]() {
+          named_barrier(1, TEAM_M);
+          if (tid == 0) {
+            if (it + 2 < n_it) issue_tma(it + 2);
+            if (it + 3 < n_it) prefetch_l2(it + 3);
+          }
+          if (it >= 1) mbar_wait(bars + 8, (unsigned)((it - 1) & 1));  // epilogue of tile it-1 read sacc
+        };
+        mma_tile_u<MODE, MAT, true, true>(p, sq_of(b), sg_of(b), sp_of(b), sr, smem_raw + BARW, nocodes, tile, g,
+                                          lane, alpha, read_res, release, flux_wait, flux_done, sacc);
+        mbar_arrive(bars + 7);  // release: the rhs of tile it is in sacc
+        continue;
+      }
+      mma_tile_u<MODE, MAT, true>(p, sq_of(b), sg_of(b), sp_of(b), sr, smem_raw + BARW, nocodes, tile, g, lane,
                                   alpha, read_res, after_lift, flux_wait, flux_done);
       named_barrier(1, TEAM_M);  // every DMMA warp is done with A[b] and sr
       if (tid == 0) {
@@ -1739,6 +1806,40 @@ __global__ void __launch_bounds__(TEAM_WS, 1) stage_kernel_ws(const dg::StageArg
     if (TMA_ST && tid == 0) bulk_wait_all();
   } else {  // ------------------------------------------------------------------ flux warps
     const int gf = g - P;
+    // WS2: LSERK4 update of tile j from sacc (rhs), q_in and the residual (global), elementwise over
+    // the tile's physical offsets (every array shares the tile layout): coalesced 16-byte accesses
+    auto epilogue = [&](int j) {
+      mbar_wait(bars + 7, (unsigned)(j & 1));
+      const int64_t t0 = (int64_t)tile_of(j) * NP * TL;
+      const T a = static_cast<T>(p.a), bb = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
+      const T* __restrict__ res = static_cast<const T*>(p.res) + t0;
+      T* __restrict__ reso = static_cast<T*>(p.res) + t0;
+      T* __restrict__ qo = static_cast<T*>(p.q_out) + t0;
+      const T* __restrict__ qi = q + t0;
+      using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+#pragma unroll 2
+      for (int o = 2 * (tid - TEAM_M); o < NP * TL; o += 2 * WF * 32) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const V2 r = *reinterpret_cast<const V2*>(sacc + c * NP * TL + o);
+          V2 rs;
+          rs.x = dt * r.x;
+          rs.y = dt * r.y;
+          if (read_res) {
+            const V2 ro = __ldcs(reinterpret_cast<const V2*>(res + c * p.vstride + o));
+            rs.x = fma(a, ro.x, rs.x);
+            rs.y = fma(a, ro.y, rs.y);
+          }
+          const V2 qv = __ldg(reinterpret_cast<const V2*>(qi + c * p.fstride + o));
+          V2 qn;
+          qn.x = fma(bb, rs.x, qv.x);
+          qn.y = fma(bb, rs.y, qv.y);
+          if (p.write_res) st_out(reinterpret_cast<V2*>(reso + c * p.vstride + o), rs);
+          st_out(reinterpret_cast<V2*>(qo + c * p.fstride + o), qn);
+        }
+      }
+      mbar_arrive(bars + 8);
+    };
     int32_t cc[KF], cn[KF];  // neighbour codes of tiles it, it+1
     auto load_codes = [&](int it, int32_t (&v)[KF]) {
       const int32_t* src = p.vmapP + (int64_t)tile_of(it) * NF * TL;
@@ -1784,9 +1885,13 @@ __global__ void __launch_bounds__(TEAM_WS, 1) stage_kernel_ws(const dg::StageArg
         sp[2 * NFE * TL + pm] = fEz;
       }
       mbar_arrive(bars + 3 + b);  // release: the flux of tile it is in F[b]
+      if constexpr (WS2) {
+        if (it >= 1) epilogue(it - 1);
+      }
 #pragma unroll
       for (int k = 0; k < KF; ++k) cc[k] = cn[k];
     }
+    if constexpr (WS2) epilogue(n_it - 1);
   }
 }
 
