@@ -70,6 +70,11 @@ constexpr size_t SMEM_SURF_Q = BARB + LVB + FMB + SPB + QB + GB;
 #define DG_SQ 1
 #endif
 constexpr bool STAGEQ = DG_SQ && SMEM_SURF_Q <= 227 * 1024;
+// DG_PF3: the surface kernel loads rhsV and the residual of its rows at the top of the tile (registers)
+#ifndef DG_PF3
+#define DG_PF3 1
+#endif
+constexpr bool PF3 = DG_PF3;
 constexpr size_t SMEM_SURF = STAGEQ ? SMEM_SURF_Q : LVB + FMB + SPB;
 static_assert(SMEM_VOL <= 227 * 1024 && SMEM_SURF <= 227 * 1024, "3D kernel shared memory");
 
@@ -247,6 +252,19 @@ __global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
     const T* qt = STAGEQ ? sq + lane : q + t * NP * TL + lane;
     const int64_t FSQ = STAGEQ ? (int64_t)NP * TL : p.fstride;
     const int32_t* codes = p.vmapP + t * NF * TL + lane;
+    // rhsV (the volume kernel's output) and the LSERK4 residual of this warp's rows: issued before the
+    // flux, so their latency hides behind the flux and the LIFT (DG_PF3; the LIFT accumulates onto rhsV)
+    T acc[6][RS], rr[6][RS];
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      const int n = n0 + r < NP ? n0 + r : NP - 1;
+      const int64_t o = (t * NP + n) * TL + lane;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        acc[c][r] = (PF3 && MODE != dg::MODE_SURFACE) ? static_cast<const T*>(p.rhsv)[c * p.vstride + o] : T(0);
+        if constexpr (PF3 && is_rk<MODE>()) rr[c][r] = read_res ? __ldcs(static_cast<const T*>(p.res) + c * p.vstride + o) : T(0);
+      }
+    }
     // flux at this warp's face points m = g + kP (compile-time trip count: the trace loads of
     // several points are in flight together)
 #pragma unroll 4
@@ -282,11 +300,6 @@ __global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
       s[5 * NF * TL] = hF * (-(nx * d[1] - ny * d[0]) + alpha * (nz * ndE - d[5]));
     }
     __syncthreads();
-    T acc[6][RS];
-#pragma unroll
-    for (int c = 0; c < 6; ++c)
-#pragma unroll
-      for (int r = 0; r < RS; ++r) acc[c][r] = T(0);
 #pragma unroll 2
     for (int m = 0; m < NF; ++m) {
       T fv[6];
@@ -310,7 +323,7 @@ __global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
         rhs[c] = acc[c][r];
-        if (MODE != dg::MODE_SURFACE) rhs[c] += static_cast<const T*>(p.rhsv)[c * p.vstride + o];
+        if (!PF3 && MODE != dg::MODE_SURFACE) rhs[c] += static_cast<const T*>(p.rhsv)[c * p.vstride + o];
       }
       if constexpr (is_rk<MODE>()) {
         T* __restrict__ res = static_cast<T*>(p.res);
@@ -318,7 +331,7 @@ __global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
           T rs = dt * rhs[c];
-          if (read_res) rs = fma(a, __ldcs(res + c * p.vstride + o), rs);
+          if (read_res) rs = fma(a, PF3 ? rr[c][r] : __ldcs(res + c * p.vstride + o), rs);
           if (p.write_res) __stcs(res + c * p.vstride + o, rs);
           __stcs(qo + c * p.fstride + o, fma(b, rs, qt[c * FSQ + n * TL]));
         }
