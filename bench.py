@@ -538,6 +538,8 @@ def bytes_3d(Np, Nfp, s, kind):
     traces are re-reads of q: L2 hits, not counted)."""
     if kind == "volume":
         return (12 * Np + 9) * s
+    if kind == "fused":  # q in / out, the residual (read on stages 1-4, written on 0-3), 9 + 20 geometry words
+        return (12 * Np + 2 * 0.8 * 6 * Np + 29) * s + 4 * Nfp * 4
     return (12 * Np + 2 * 0.8 * 6 * Np + 20) * s + 4 * Nfp * 4
 
 
@@ -545,13 +547,16 @@ def flops_3d(N, kind):
     Np, Nfp = (N + 1) * (N + 2) * (N + 3) // 6, (N + 1) * (N + 2) // 2
     if kind == "volume":
         return 2 * 18 * Np * Np + 36 * 2 * Np   # 18 mat-vecs + the chain-rule combinations
+    if kind == "fused":
+        return flops_3d(N, "volume") + flops_3d(N, "surface")
     NF = 4 * Nfp
     return 2 * 6 * Np * NF + NF * 6 * 12 + 6 * Np * 5  # LIFT of 6 fields + flux + rhsV add and LSERK4
 
 
 def run_3d(args):
     """The 3D tetrahedral Maxwell step (config 'hedge3d'): PEC unit cube, n^3 cells x 6 Kuhn tetrahedra,
-    the (1,1,1) cavity mode, LSERK4; one step = 5 stages x (volume kernel + surface/LIFT/RK kernel)."""
+    the (1,1,1) cavity mode, LSERK4; one step = 5 stages x (the fused stage kernel, or with --split /
+    where the fused tile does not fit: volume kernel + surface/LIFT/RK kernel)."""
     import torch
 
     from paper_1304_5546_b200 import dg3
@@ -560,7 +565,7 @@ def run_3d(args):
     N, n, prec = args.order, args.n, args.prec
     VX, VY, VZ, E = dginputs.cube_tet_mesh(n)
     K = E.shape[0]
-    c = dg3.dg3_setup(N, VX, VY, VZ, E, precision=prec)
+    c = dg3.dg3_setup(N, VX, VY, VZ, E, precision=prec, fused=not args.split)
     Np, Nfp = c.Np, c.Nfp
     x, y, z = c.nodes()
     c.set_fields(*dginputs.cube_cavity_mode(x, y, z, 0.0))
@@ -589,7 +594,8 @@ def run_3d(args):
     hbm, peak_src = peaks()
     s = prec
     roofs = {}
-    for kind in ("volume", "surface"):
+    kinds = [k for k in ("fused", "volume", "surface") if st[k]["timed"] > 0]
+    for kind in kinds:
         k_ms = st[kind]["ms"] / (5 * prof)
         ab = bytes_3d(Np, Nfp, s, kind) * K
         fl = flops_3d(N, kind) * K
@@ -602,7 +608,9 @@ def run_3d(args):
                            flops_per_launch=fl, achieved_gflops=tfl * 1e3,
                            other_roof={k: alt[k] for k in ("bound", "achieved", "peak", "unit", "frac")})
     dom = max(roofs, key=lambda k: roofs[k]["avg_launch_ms"])
-    roof = dict(roofs[dom], second_kernel=roofs["volume" if dom == "surface" else "surface"])
+    roof = dict(roofs[dom])
+    if len(roofs) > 1:
+        roof["second_kernel"] = roofs["volume" if dom == "surface" else "surface"]
     # e2e through the public API: set fields (host fp64), K steps, get fields
     host = [np.ascontiguousarray(a) for a in dginputs.cube_cavity_mode(x, y, z, 0.0)]
     t0e = time.perf_counter()
@@ -619,7 +627,9 @@ def run_3d(args):
             "scaling": "none", "vs_baseline": None, "dtype": "f32" if prec == 4 else "f64", "data": "synthetic",
             "config": {"workload": f"hedge3d: 3D TM/TE Maxwell PEC unit cube, N={N}, K={K:,} tetrahedra "
                                    f"({n}^3 cells x 6), {'fp32' if prec == 4 else 'fp64'}, LSERK4, cavity mode (1,1,1)",
-                       "N": N, "K": K, "Np": Np, "kernels": "volume (18 mat-vecs) + surface/LIFT/LSERK4 (FMA)",
+                       "N": N, "K": K, "Np": Np,
+                       "kernels": ("fused stage: volume (18 mat-vecs) + flux + LIFT + LSERK4 (FMA)" if kinds == ["fused"]
+                                   else "volume (18 mat-vecs) + surface/LIFT/LSERK4 (FMA)"),
                        "l2": f"no flush: working set {(9 * K * Np * s) / 1e6:.0f} MB"},
             "gflops": flops_step / (ms / args.steps * 1e-3) / 1e9,
             "roofline": roof, "cpu_baseline": None,

@@ -37,8 +37,10 @@ typedef struct dg3_ctx dg3_ctx;
 #define DG3_MAX_KERNEL_N 5
 
 /* Build a 3D context.  options: abi_version, N (setup 1..15, kernels 1..DG3_MAX_KERNEL_N),
- * precision (4|8), device, alpha, stream, max_ctas are used; rank/nranks must be 0/1; the other
- * fields are ignored.  VX, VY, VZ [Nv] (host fp64), EToV [K][4] (host int64, 0-based). */
+ * precision (4|8), device, alpha, stream, max_ctas and fused are used (fused = 1: one fused stage
+ * kernel -- volume, flux, LIFT and LSERK4 update -- per stage wherever its tile fits in shared memory,
+ * else, and with fused = 0, the volume kernel then the surface+LIFT+RK kernel); rank/nranks must be
+ * 0/1; the other fields are ignored.  VX, VY, VZ [Nv] (host fp64), EToV [K][4] (host int64, 0-based). */
 dg_status dg3_setup(const dg_options* opts, int64_t Nv, const double* VX, const double* VY, const double* VZ,
                     int64_t K, const int64_t* EToV, dg3_ctx** out);
 

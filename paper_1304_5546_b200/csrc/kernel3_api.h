@@ -32,6 +32,8 @@ struct KernelInfo3 {
   int N, prec, threads, rows_per_warp;
   size_t smem_volume, smem_surface;
   int staged;  // 1: the surface kernel stages the tile's fields in shared memory
+  int fused;   // 1: the fused stage kernel (MODE_FUSED_RK) exists for this (N, precision)
+  size_t smem_fused;
 };
 
 struct KernelModule3 {
@@ -40,12 +42,15 @@ struct KernelModule3 {
   void (*pack_ops)(const double* Dr, const double* Ds, const double* Dt, const double* LIFT, const int* Fmask,
                    void* out) = nullptr;
   // mode: MODE_VOLUME (K1 -> out), MODE_SURFACE_RK (K2 + rhsv -> LSERK4), MODE_RHS (K2 + rhsv -> out),
-  // MODE_SURFACE (K2 alone -> out)
+  // MODE_SURFACE (K2 alone -> out), MODE_FUSED_RK (the fused stage kernel, when `fused`)
   cudaError_t (*launch)(int mode, const StageArgs3& a, cudaStream_t s) = nullptr;
   KernelInfo3 (*info)() = nullptr;
   // 1: the surface kernel stages the tile's fields in shared memory, so a neighbour node in the same
   // 32-element tile is coded as a shared-memory offset: vmapP code = -(1 + n * 32 + lane)
   int staged = 0;
+  // 1: MODE_FUSED_RK runs the fused stage kernel (volume + flux + LIFT + LSERK4 in one launch; it
+  // always stages the tile's fields, so the runtime codes same-tile neighbours as shared offsets)
+  int fused = 0;
 };
 
 const KernelModule3* find_module3(int N, int prec);

@@ -52,10 +52,20 @@ constexpr int PS = (NP + RS - 1) / RS;
 constexpr int RPS = PS * RS;
 constexpr int TEAMS = 32 * PS;
 constexpr int KPT = (NF + PS - 1) / PS;    // face points per warp (surface kernel)
+// fused stage kernel: its own rows per warp (volume + LIFT accumulators and the residual in registers)
+#ifndef DG_RF
+#define DG_RF 4
+#endif
+constexpr int RF = DG_RF * 32 >= NP ? DG_RF : (NP + 31) / 32;
+constexpr int PF = (NP + RF - 1) / RF;
+constexpr int RPF = PF * RF;
+constexpr int TEAMF = 32 * PF;
+constexpr int RPD = RP > RPF ? RP : RPF;  // operator-row padding of DV (volume and fused kernels)
 // operator block: DV[j][n] = {Dr, Ds, Dt, 0} [NP][RP], LV[m][n] [NF][RP], fmask [NF] int32
 struct alignas(4 * sizeof(T)) T4 { T x, y, z, w; };
-constexpr size_t DVB = (size_t)NP * RP * sizeof(T4);
-constexpr size_t LVB = (size_t)NF * RPS * sizeof(T);
+constexpr size_t DVB = (size_t)NP * RPD * sizeof(T4);
+constexpr int RPM = (RP > RPS ? RP : RPS) > RPF ? (RP > RPS ? RP : RPS) : RPF;  // LIFT row padding (all kernels)
+constexpr size_t LVB = (size_t)NF * RPM * sizeof(T);
 constexpr size_t FMB = ((size_t)NF * 4 + 15) / 16 * 16;
 constexpr size_t OPS = DVB + LVB + FMB;
 constexpr size_t QB = (size_t)6 * NP * TL * sizeof(T);
@@ -77,6 +87,12 @@ constexpr bool STAGEQ = DG_SQ && SMEM_SURF_Q <= 227 * 1024;
 constexpr bool PF3 = DG_PF3;
 constexpr size_t SMEM_SURF = STAGEQ ? SMEM_SURF_Q : LVB + FMB + SPB;
 static_assert(SMEM_VOL <= 227 * 1024 && SMEM_SURF <= 227 * 1024, "3D kernel shared memory");
+// fused stage kernel (volume + flux + LIFT + LSERK4, one launch per stage) when its tile fits
+constexpr size_t SMEM_FUSED = BARB + DVB + LVB + FMB + QB + GB + SPB;
+#ifndef DG_F3
+#define DG_F3 1
+#endif
+constexpr bool FUSED3 = DG_F3 && SMEM_FUSED <= 227 * 1024;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -176,7 +192,7 @@ __global__ void __launch_bounds__(TEAM, 1) volume3d(const dg::StageArgs3 p) {
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const T4 d = DV[j * RP + n0 + r];
+        const T4 d = DV[j * RPD + n0 + r];
 #pragma unroll
         for (int c = 0; c < 6; ++c) acc[c][r] = fma(d.x, W[c][0], fma(d.y, W[c][1], fma(d.z, W[c][2], acc[c][r])));
       }
@@ -307,7 +323,7 @@ __global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
       for (int c = 0; c < 6; ++c) fv[c] = sp[(c * NF + m) * TL + lane];
 #pragma unroll
       for (int r = 0; r < RS; ++r) {
-        const T l = LV[m * RPS + n0 + r];
+        const T l = LV[m * RPM + n0 + r];
 #pragma unroll
         for (int c = 0; c < 6; ++c) acc[c][r] = fma(l, fv[c], acc[c][r]);
       }
@@ -350,6 +366,173 @@ __global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
   }
 }
 
+
+// ---------------------------------------------------------------- fused stage: K1 + K2 + LSERK4
+// One launch per LSERK4 stage: per tile the fields and geometry arrive by
+// TMA; the volume curl (as volume3d) and the LIFT of the flux (as surface3d) accumulate into the same
+// registers (warp g: rows [gR, gR + R)); the flux of this warp's face points m = g + kP reads own and
+// same-tile neighbour traces from shared memory, other neighbours from global memory / L2; the
+// LSERK4 residual of the warp's rows is loaded at the top of the tile.  No rhsV round trip.
+__global__ void __launch_bounds__(TEAMF, 1) fused3d(const dg::StageArgs3 p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  const T4* DV = reinterpret_cast<const T4*>(smem_raw + BARB);
+  const T* LV = reinterpret_cast<const T*>(smem_raw + BARB + DVB);
+  const int32_t* fmask = reinterpret_cast<const int32_t*>(smem_raw + BARB + DVB + LVB);
+  T* sq = reinterpret_cast<T*>(smem_raw + BARB + DVB + LVB + FMB);
+  T* sg = reinterpret_cast<T*>(smem_raw + BARB + DVB + LVB + FMB + QB);
+  T* sp = reinterpret_cast<T*>(smem_raw + BARB + DVB + LVB + FMB + QB + GB);
+  const T* __restrict__ q = static_cast<const T*>(p.q_in);
+  const T* __restrict__ geo = static_cast<const T*>(p.geo);
+  const int tid = threadIdx.x, g = tid >> 5, lane = tid & 31, n0 = g * RF;
+  const int first = blockIdx.x, stride = gridDim.x;
+  const int n_it = first < p.ntiles ? (p.ntiles - first + stride - 1) / stride : 0;
+  if (n_it == 0) return;
+  constexpr int KPF = (NF + PF - 1) / PF;  // face points per warp
+  auto issue = [&](int it) {
+    if (tid == 0) {
+      const int64_t t = first + (int64_t)it * stride;
+      mbar_expect_tx(bar, (unsigned)(QB + GB));
+#pragma unroll
+      for (int c = 0; c < 6; ++c)
+        tma_load_1d(sq + c * NP * TL, q + c * p.fstride + t * NP * TL, (unsigned)(NP * TL * sizeof(T)), bar);
+      tma_load_1d(sg, geo + t * NG * TL, (unsigned)GB, bar);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  {
+    const int4* src = reinterpret_cast<const int4*>(p.ops);
+    int4* dst = reinterpret_cast<int4*>(smem_raw + BARB);
+    for (int i = tid; i < (int)((DVB + LVB + FMB) / 16); i += TEAMF) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  issue(0);
+  const T alpha = static_cast<T>(p.alpha);
+  const bool read_res = p.a != 0.0;
+  const T a = static_cast<T>(p.a), b = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
+  for (int it = 0; it < n_it; ++it) {
+    const int64_t t = first + (int64_t)it * stride;
+    mbar_wait(bar, (unsigned)(it & 1));
+    __syncthreads();
+    if (it + 1 < n_it && tid == 0) {
+      const int64_t t1 = t + stride;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) prefetch_l2(q + c * p.fstride + t1 * NP * TL, (unsigned)(NP * TL * sizeof(T)));
+      prefetch_l2(geo + t1 * NG * TL, (unsigned)GB);
+    }
+    // the LSERK4 residual of this warp's rows (in flight during the volume and surface phases)
+    T rr[6][RF];
+#pragma unroll
+    for (int r = 0; r < RF; ++r) {
+      const int n = n0 + r < NP ? n0 + r : NP - 1;
+      const int64_t o = (t * NP + n) * TL + lane;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) rr[c][r] = read_res ? __ldcs(static_cast<const T*>(p.res) + c * p.vstride + o) : T(0);
+    }
+    const T* gg = sg + lane;
+    T acc[6][RF];
+    {  // volume: acc = (-curl E, curl H) of rows n0 .. n0 + R - 1 (volume3d's regrouped chain rule)
+      const T rx = gg[0 * TL], ry = gg[1 * TL], rz = gg[2 * TL], sx = gg[3 * TL], sy = gg[4 * TL], sz = gg[5 * TL],
+              tx = gg[6 * TL], ty = gg[7 * TL], tz = gg[8 * TL];
+#pragma unroll
+      for (int c = 0; c < 6; ++c)
+#pragma unroll
+        for (int r = 0; r < RF; ++r) acc[c][r] = T(0);
+#pragma unroll 2
+      for (int j = 0; j < NP; ++j) {
+        const T* col = sq + j * TL + lane;
+        const T Hx = col[0 * NP * TL], Hy = col[1 * NP * TL], Hz = col[2 * NP * TL];
+        const T Ex = col[3 * NP * TL], Ey = col[4 * NP * TL], Ez = col[5 * NP * TL];
+        T W[6][3];
+        const T dxv[3] = {rx, sx, tx}, dyv[3] = {ry, sy, ty}, dzv[3] = {rz, sz, tz};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          W[0][d] = dzv[d] * Ey - dyv[d] * Ez;  // -(curl E)  -> dH/dt
+          W[1][d] = dxv[d] * Ez - dzv[d] * Ex;
+          W[2][d] = dyv[d] * Ex - dxv[d] * Ey;
+          W[3][d] = dyv[d] * Hz - dzv[d] * Hy;  // curl H -> dE/dt
+          W[4][d] = dzv[d] * Hx - dxv[d] * Hz;
+          W[5][d] = dxv[d] * Hy - dyv[d] * Hx;
+        }
+#pragma unroll
+        for (int r = 0; r < RF; ++r) {
+          const T4 d = DV[j * RPD + n0 + r];
+#pragma unroll
+          for (int c = 0; c < 6; ++c) acc[c][r] = fma(d.x, W[c][0], fma(d.y, W[c][1], fma(d.z, W[c][2], acc[c][r])));
+        }
+      }
+    }
+    // flux of this warp's face points into sp (surface3d's upwind flux, 1/2 of the jump form)
+    const int32_t* codes = p.vmapP + t * NF * TL + lane;
+#pragma unroll 4
+    for (int k = 0; k < KPF; ++k) {
+      const int m = g + k * PF;
+      if (m >= NF) break;
+      const int f = m / NFP;
+      const int fm = fmask[m];
+      const int32_t code = __ldg(codes + m * TL);
+      const T* pn = code >= 0 ? q + code : sq + (-1 - code);
+      const int64_t fsn = code >= 0 ? p.fstride : (int64_t)NP * TL;
+      T own[6], nb[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        own[c] = sq[c * NP * TL + fm * TL + lane];
+        nb[c] = pn[c * fsn];
+      }
+      const T nx = gg[(9 + 4 * f) * TL], ny = gg[(10 + 4 * f) * TL], nz = gg[(11 + 4 * f) * TL];
+      const T hF = gg[(12 + 4 * f) * TL], bsc = gg[(25 + f) * TL];
+      T d[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) d[c] = c < 3 ? (bsc < T(0) ? T(0) : own[c] - nb[c]) : own[c] - bsc * nb[c];
+      const T ndH = nx * d[0] + ny * d[1] + nz * d[2];
+      const T ndE = nx * d[3] + ny * d[4] + nz * d[5];
+      T* s = sp + m * TL + lane;
+      s[0 * NF * TL] = hF * ((ny * d[5] - nz * d[4]) + alpha * (nx * ndH - d[0]));
+      s[1 * NF * TL] = hF * ((nz * d[3] - nx * d[5]) + alpha * (ny * ndH - d[1]));
+      s[2 * NF * TL] = hF * ((nx * d[4] - ny * d[3]) + alpha * (nz * ndH - d[2]));
+      s[3 * NF * TL] = hF * (-(ny * d[2] - nz * d[1]) + alpha * (nx * ndE - d[3]));
+      s[4 * NF * TL] = hF * (-(nz * d[0] - nx * d[2]) + alpha * (ny * ndE - d[4]));
+      s[5 * NF * TL] = hF * (-(nx * d[1] - ny * d[0]) + alpha * (nz * ndE - d[5]));
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int m = 0; m < NF; ++m) {  // LIFT onto the volume term
+      T fv[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) fv[c] = sp[(c * NF + m) * TL + lane];
+#pragma unroll
+      for (int r = 0; r < RF; ++r) {
+        const T l = LV[m * RPM + n0 + r];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) acc[c][r] = fma(l, fv[c], acc[c][r]);
+      }
+    }
+    // LSERK4 update (q_in from shared memory), streaming stores
+    T* __restrict__ res = static_cast<T*>(p.res);
+    T* __restrict__ qo = static_cast<T*>(p.q_out);
+#pragma unroll
+    for (int r = 0; r < RF; ++r) {
+      const int n = n0 + r;
+      if (RPF != NP && n >= NP) break;
+      const int64_t o = (t * NP + n) * TL + lane;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        T rs = dt * acc[c][r];
+        if (read_res) rs = fma(a, rr[c][r], rs);
+        if (p.write_res) __stcs(res + c * p.vstride + o, rs);
+        __stcs(qo + c * p.fstride + o, fma(b, rs, sq[(c * NP + n) * TL + lane]));
+      }
+    }
+    if (it + 1 < n_it) {
+      __syncthreads();  // every thread is done with the tile's fields and flux
+      issue(it + 1);
+    }
+  }
+}
+
 template <typename KER>
 cudaError_t launch_k(KER kernel, size_t smem, int team, const dg::StageArgs3& a, cudaStream_t s, int* cap) {
   int dev = 0;
@@ -372,8 +555,11 @@ cudaError_t launch_k(KER kernel, size_t smem, int team, const dg::StageArgs3& a,
 }
 
 cudaError_t launch(int mode, const dg::StageArgs3& a, cudaStream_t s) {
-  static int cap_v[64] = {0}, cap_rk[64] = {0}, cap_rhs[64] = {0}, cap_s[64] = {0};
+  static int cap_v[64] = {0}, cap_rk[64] = {0}, cap_rhs[64] = {0}, cap_s[64] = {0}, cap_f[64] = {0};
   switch (mode) {
+    case dg::MODE_FUSED_RK:
+      if constexpr (FUSED3) return launch_k(fused3d, SMEM_FUSED, TEAMF, a, s, cap_f);
+      return cudaErrorNotSupported;
     case dg::MODE_VOLUME: return launch_k(volume3d, SMEM_VOL, TEAM, a, s, cap_v);
     case dg::MODE_SURFACE_RK: return launch_k(surface3d<dg::MODE_SURFACE_RK>, SMEM_SURF, TEAMS, a, s, cap_rk);
     case dg::MODE_RHS: return launch_k(surface3d<dg::MODE_RHS>, SMEM_SURF, TEAMS, a, s, cap_rhs);
@@ -389,14 +575,14 @@ void pack_ops(const double* Dr, const double* Ds, const double* Dt, const double
   T4* dv = reinterpret_cast<T4*>(o);
   for (int j = 0; j < NP; ++j)
     for (int n = 0; n < NP; ++n) {
-      T4& e = dv[j * RP + n];
+      T4& e = dv[j * RPD + n];
       e.x = static_cast<T>(Dr[n * NP + j]);
       e.y = static_cast<T>(Ds[n * NP + j]);
       e.z = static_cast<T>(Dt[n * NP + j]);
     }
   T* lv = reinterpret_cast<T*>(o + DVB);
   for (int m = 0; m < NF; ++m)
-    for (int n = 0; n < NP; ++n) lv[m * RPS + n] = static_cast<T>(LIFT[n * NF + m]);
+    for (int n = 0; n < NP; ++n) lv[m * RPM + n] = static_cast<T>(LIFT[n * NF + m]);
   int32_t* fm = reinterpret_cast<int32_t*>(o + DVB + LVB);
   for (int m = 0; m < NF; ++m) fm[m] = Fmask[m];
 }
@@ -410,6 +596,8 @@ dg::KernelInfo3 info() {
   k.smem_volume = SMEM_VOL;
   k.smem_surface = SMEM_SURF;
   k.staged = STAGEQ ? 1 : 0;
+  k.fused = FUSED3 ? 1 : 0;
+  k.smem_fused = FUSED3 ? SMEM_FUSED : 0;
   return k;
 }
 
@@ -425,6 +613,7 @@ KernelModule3 DG_CAT(dg_module3_, DG_TAG)() {
   m.launch = &launch;
   m.info = &info;
   m.staged = STAGEQ ? 1 : 0;
+  m.fused = FUSED3 ? 1 : 0;
   return m;
 }
 }  // namespace dg

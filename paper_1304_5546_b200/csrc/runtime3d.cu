@@ -130,6 +130,7 @@ std::vector<int64_t> morton_order3(const dg::Mesh3D& m) {
 
 struct dg3_ctx {
   int N = 0, prec = 8, device = -1, max_ctas = 0;
+  bool fused = false;  // the fused stage kernel (dg_options.fused and the module has one)
   double alpha = 1.0;
   bool host_only = true, poisoned = false;
   dg::RefTet ref;
@@ -224,8 +225,12 @@ dg_status stage3(dg3_ctx* c, int i, double dt) {
   dg::StageArgs3 av = a;
   av.out = c->rhsv;
   dg_status st;
-  if ((st = launch3(c, dg::MODE_VOLUME, av, 1)) != DG_OK) return st;
-  if ((st = launch3(c, dg::MODE_SURFACE_RK, a, 2)) != DG_OK) return st;
+  if (c->fused) {  // volume + flux + LIFT + LSERK4 in one launch
+    if ((st = launch3(c, dg::MODE_FUSED_RK, a, 0)) != DG_OK) return st;
+  } else {
+    if ((st = launch3(c, dg::MODE_VOLUME, av, 1)) != DG_OK) return st;
+    if ((st = launch3(c, dg::MODE_SURFACE_RK, a, 2)) != DG_OK) return st;
+  }
   c->cur = 1 - c->cur;
   return DG_OK;
 }
@@ -283,6 +288,7 @@ dg_status setup_device3(dg3_ctx* c, const dg_options* o) {
   if (c->device >= ndev) return err3(DG_E_ARG, "device ordinal out of range");
   CU3(c, cudaSetDevice(c->device));
   c->km = dg::find_module3(c->N, c->prec);
+  if (c->km && !c->km->fused) c->fused = false;
   if (!c->km) return err3(DG_E_DEGREE, "no 3D kernel module for N=" + std::to_string(c->N) + " precision=" +
                                            std::to_string(c->prec));
   const int Np = c->ref.Np;
@@ -371,6 +377,7 @@ dg_status dg3_setup(const dg_options* o, int64_t Nv, const double* VX, const dou
   c->device = o->device;
   c->alpha = o->alpha;
   c->max_ctas = o->max_ctas;
+  c->fused = o->fused != 0;  // effective only where the module has a fused kernel (setup_device3)
   try {
     c->ref = dg::build_reftet(o->N);
     dg::build_mesh3d(c->ref, Nv, VX, VY, VZ, K, EToV, c->mesh);
@@ -479,8 +486,12 @@ dg_status dg3_run(dg3_ctx* c, double dt, int64_t nsteps) {
         if (e2 != cudaSuccess) return cuda3(c, e2, "cudaGraphInstantiate");
       }
       CU3(c, cudaGraphLaunch(c->gexec[par], c->stream));
-      c->stats.launches[1] += 5;
-      c->stats.launches[2] += 5;
+      if (c->fused) {
+        c->stats.launches[0] += 5;
+      } else {
+        c->stats.launches[1] += 5;
+        c->stats.launches[2] += 5;
+      }
       c->cur = 1 - c->cur;
     } else {
       for (int i = 0; i < 5; ++i)

@@ -156,8 +156,9 @@ class Context3:
         return {k: dict(launches=st.launches[i], ms=st.ms[i], timed=st.timed[i]) for i, k in enumerate(_dg.KIND)}
 
 
-def dg3_setup(N, VX, VY, VZ, EToV, precision=8, device=0, alpha=1.0, stream=None, max_ctas=0):
-    """dg3_setup: a single-GPU 3D context on the tetrahedral mesh (VX, VY, VZ, EToV [K][4])."""
+def dg3_setup(N, VX, VY, VZ, EToV, precision=8, device=0, alpha=1.0, stream=None, max_ctas=0, fused=True):
+    """dg3_setup: a single-GPU 3D context on the tetrahedral mesh (VX, VY, VZ, EToV [K][4]);
+    fused: one fused stage kernel per LSERK4 stage where compiled, else volume + surface kernels."""
     VX, VY, VZ = (_dg._as(a, np.float64) for a in (VX, VY, VZ))
     EToV = _dg._as(EToV, np.int64)
     K = EToV.shape[0]
@@ -167,6 +168,7 @@ def dg3_setup(N, VX, VY, VZ, EToV, precision=8, device=0, alpha=1.0, stream=None
     o.N, o.precision, o.device, o.alpha = int(N), int(precision), int(device), float(alpha)
     o.stream = stream
     o.max_ctas = int(max_ctas)
+    o.fused = 1 if fused else 0
     h = C.c_void_p()
     _check(_lib.dg3_setup(C.byref(o), VX.size, _ptr(VX), _ptr(VY), _ptr(VZ), K, _ptr(EToV), C.byref(h)))
     return Context3(h.value, int(N), int(precision))

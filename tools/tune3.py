@@ -22,7 +22,9 @@ GRID = [dict(SQ=sq, RS=rs) for sq, rs in itertools.product((0, 1), (2, 4, 8))]
 GRID2 = [dict(SQ=sq, RS=1) for sq in (0, 1)] + [dict(SQ=sq, RS=2, R=r) for sq, r in itertools.product((0, 1), (4, 16))]
 # third pass: RS = 1 (N <= 3 picks) and RS = 4 (N = 4 fp32 pick) with the volume R
 GRID3 = [dict(SQ=sq, RS=1, R=r) for sq, r in itertools.product((0, 1), (4, 16))] + [dict(SQ=1, RS=4, R=r) for r in (4, 16)]
-GRID = {"2": GRID2, "3": GRID3}.get(os.environ.get("TUNE3_GRID", ""), GRID)
+# fused-stage pass (round 2): the fused kernel's rows per warp RF (its other knobs are RF-only)
+GRIDF = [dict(RF=r) for r in (1, 2, 4, 8)]
+GRID = {"2": GRID2, "3": GRID3, "fused": GRIDF}.get(os.environ.get("TUNE3_GRID", ""), GRID)
 
 
 def name(k):
