@@ -60,6 +60,13 @@ constexpr int RF = DG_RF * 32 >= NP ? DG_RF : (NP + 31) / 32;
 constexpr int PF = (NP + RF - 1) / RF;
 constexpr int RPF = PF * RF;
 constexpr int TEAMF = 32 * PF;
+// DG_VS (fused kernel): the volume term by the 18 derivative sums D_d F_c of each output row (18 FMAs per
+// operator entry, the chain rule applied once per row) instead of the regrouped W form, whose 36
+// geometry products per node column every warp repeats
+#ifndef DG_VS
+#define DG_VS 1
+#endif
+constexpr bool VSUM = DG_VS;
 constexpr int RPD = RP > RPF ? RP : RPF;  // operator-row padding of DV (volume and fused kernels)
 // operator block: DV[j][n] = {Dr, Ds, Dt, 0} [NP][RP], LV[m][n] [NF][RP], fmask [NF] int32
 struct alignas(4 * sizeof(T)) T4 { T x, y, z, w; };
@@ -434,7 +441,47 @@ __global__ void __launch_bounds__(TEAMF, 1) fused3d(const dg::StageArgs3 p) {
     }
     const T* gg = sg + lane;
     T acc[6][RF];
-    {  // volume: acc = (-curl E, curl H) of rows n0 .. n0 + R - 1 (volume3d's regrouped chain rule)
+    if constexpr (VSUM) {  // volume by derivative sums: S[d][c] = D_d F_c per row, chain rule per row
+      T S[3][6][RF];
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+#pragma unroll
+          for (int r = 0; r < RF; ++r) S[d][c][r] = T(0);
+#pragma unroll 2
+      for (int j = 0; j < NP; ++j) {
+        const T* col = sq + j * TL + lane;
+        T F[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) F[c] = col[c * NP * TL];
+#pragma unroll
+        for (int r = 0; r < RF; ++r) {
+          const T4 dd = DV[j * RPD + n0 + r];
+#pragma unroll
+          for (int c = 0; c < 6; ++c) {
+            S[0][c][r] = fma(dd.x, F[c], S[0][c][r]);
+            S[1][c][r] = fma(dd.y, F[c], S[1][c][r]);
+            S[2][c][r] = fma(dd.z, F[c], S[2][c][r]);
+          }
+        }
+      }
+      const T dxv[3] = {gg[0 * TL], gg[3 * TL], gg[6 * TL]}, dyv[3] = {gg[1 * TL], gg[4 * TL], gg[7 * TL]},
+              dzv[3] = {gg[2 * TL], gg[5 * TL], gg[8 * TL]};
+#pragma unroll
+      for (int r = 0; r < RF; ++r) {
+        // d/dx F_c = sum_d dx_d S[d][c] (eq. 6's chain rule, 3D); fields Hx Hy Hz Ex Ey Ez = 0..5
+        auto Dx = [&](int c) { return dxv[0] * S[0][c][r] + dxv[1] * S[1][c][r] + dxv[2] * S[2][c][r]; };
+        auto Dy = [&](int c) { return dyv[0] * S[0][c][r] + dyv[1] * S[1][c][r] + dyv[2] * S[2][c][r]; };
+        auto Dz = [&](int c) { return dzv[0] * S[0][c][r] + dzv[1] * S[1][c][r] + dzv[2] * S[2][c][r]; };
+        acc[0][r] = Dz(4) - Dy(5);  // dHx/dt = -(curl E)_x
+        acc[1][r] = Dx(5) - Dz(3);
+        acc[2][r] = Dy(3) - Dx(4);
+        acc[3][r] = Dy(2) - Dz(1);  // dEx/dt = (curl H)_x
+        acc[4][r] = Dz(0) - Dx(2);
+        acc[5][r] = Dx(1) - Dy(0);
+      }
+    } else {  // volume: acc = (-curl E, curl H) of rows n0 .. n0 + R - 1 (volume3d's regrouped chain rule)
       const T rx = gg[0 * TL], ry = gg[1 * TL], rz = gg[2 * TL], sx = gg[3 * TL], sy = gg[4 * TL], sz = gg[5 * TL],
               tx = gg[6 * TL], ty = gg[7 * TL], tz = gg[8 * TL];
 #pragma unroll

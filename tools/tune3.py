@@ -24,7 +24,9 @@ GRID2 = [dict(SQ=sq, RS=1) for sq in (0, 1)] + [dict(SQ=sq, RS=2, R=r) for sq, r
 GRID3 = [dict(SQ=sq, RS=1, R=r) for sq, r in itertools.product((0, 1), (4, 16))] + [dict(SQ=1, RS=4, R=r) for r in (4, 16)]
 # fused-stage pass (round 2): the fused kernel's rows per warp RF (its other knobs are RF-only)
 GRIDF = [dict(RF=r) for r in (1, 2, 4, 8)]
-GRID = {"2": GRID2, "3": GRID3, "fused": GRIDF}.get(os.environ.get("TUNE3_GRID", ""), GRID)
+# the fused kernel's volume by derivative sums (VS = 1) against the W form (VS = 0)
+GRIDV = [dict(VS=v, RF=r) for v in (0, 1) for r in (1, 2, 4)]
+GRID = {"2": GRID2, "3": GRID3, "fused": GRIDF, "vs": GRIDV}.get(os.environ.get("TUNE3_GRID", ""), GRID)
 
 
 def name(k):
