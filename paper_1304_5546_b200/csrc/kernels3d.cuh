@@ -67,6 +67,11 @@ constexpr int TEAMF = 32 * PF;
 #define DG_VS 1
 #endif
 constexpr bool VSUM = DG_VS;
+#ifndef DG_VSV
+#define DG_VSV 0  // the same for the volume kernel (split stages, dg3_eval_rhs); off: at fp64 N = 5,
+                  // the one tuned case that runs it, its 18 R sums spill
+#endif
+constexpr bool VSUMV = DG_VSV;
 constexpr int RPD = RP > RPF ? RP : RPF;  // operator-row padding of DV (volume and fused kernels)
 // operator block: DV[j][n] = {Dr, Ds, Dt, 0} [NP][RP], LV[m][n] [NF][RP], fmask [NF] int32
 struct alignas(4 * sizeof(T)) T4 { T x, y, z, w; };
@@ -127,6 +132,53 @@ __device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
 template <int MODE>
 __host__ __device__ constexpr bool is_rk() { return MODE == dg::MODE_FUSED_RK || MODE == dg::MODE_SURFACE_RK; }
 
+// Volume term by derivative sums (DG_VS): for each of the RR output rows n0 + r, S[d][c] = (D_d F_c)(n)
+// over the tile's staged fields (18 FMAs per operator entry), then the chain rule once per row:
+// acc = (-curl E, curl H) = (dH/dt, dE/dt), fields Hx Hy Hz Ex Ey Ez = 0..5
+template <int RR>
+__device__ __forceinline__ void volume_sums(const T* __restrict__ sq, const T4* __restrict__ DV, const T* __restrict__ gg,
+                                          int n0, int lane, T (&acc)[6][RR]) {
+  T S[3][6][RR];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+#pragma unroll
+      for (int r = 0; r < RR; ++r) S[d][c][r] = T(0);
+#pragma unroll 2
+  for (int j = 0; j < NP; ++j) {
+    const T* col = sq + j * TL + lane;
+    T F[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) F[c] = col[c * NP * TL];
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
+      const T4 dd = DV[j * RPD + n0 + r];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        S[0][c][r] = fma(dd.x, F[c], S[0][c][r]);
+        S[1][c][r] = fma(dd.y, F[c], S[1][c][r]);
+        S[2][c][r] = fma(dd.z, F[c], S[2][c][r]);
+      }
+    }
+  }
+  const T dxv[3] = {gg[0 * TL], gg[3 * TL], gg[6 * TL]}, dyv[3] = {gg[1 * TL], gg[4 * TL], gg[7 * TL]},
+          dzv[3] = {gg[2 * TL], gg[5 * TL], gg[8 * TL]};
+#pragma unroll
+  for (int r = 0; r < RR; ++r) {
+    // d/dx F_c = sum_d dx_d S[d][c] (eq. 6's chain rule, 3D); fields Hx Hy Hz Ex Ey Ez = 0..5
+    auto Dx = [&](int c) { return dxv[0] * S[0][c][r] + dxv[1] * S[1][c][r] + dxv[2] * S[2][c][r]; };
+    auto Dy = [&](int c) { return dyv[0] * S[0][c][r] + dyv[1] * S[1][c][r] + dyv[2] * S[2][c][r]; };
+    auto Dz = [&](int c) { return dzv[0] * S[0][c][r] + dzv[1] * S[1][c][r] + dzv[2] * S[2][c][r]; };
+    acc[0][r] = Dz(4) - Dy(5);  // dHx/dt = -(curl E)_x
+    acc[1][r] = Dx(5) - Dz(3);
+    acc[2][r] = Dy(3) - Dx(4);
+    acc[3][r] = Dy(2) - Dz(1);  // dEx/dt = (curl H)_x
+    acc[4][r] = Dz(0) - Dx(2);
+    acc[5][r] = Dx(1) - Dy(0);
+  }
+}
+
 // ---------------------------------------------------------------- K1: volume (curl) kernel
 __global__ void __launch_bounds__(TEAM, 1) volume3d(const dg::StageArgs3 p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -172,6 +224,22 @@ __global__ void __launch_bounds__(TEAM, 1) volume3d(const dg::StageArgs3 p) {
     }
     const int64_t t = first + (int64_t)it * stride;
     const T* gg = sg + lane;
+    if constexpr (VSUMV) {  // derivative sums (volume_sums): acc = (dH/dt, dE/dt) directly
+      T acc[6][R];
+      volume_sums<R>(sq, DV, gg, n0, lane, acc);
+      __syncthreads();  // every warp is done with the tile's fields: the next TMA may overwrite them
+      if (it + 1 < n_it) issue(it + 1);
+      T* __restrict__ out = static_cast<T*>(p.out);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int n = n0 + r;
+        if (RP != NP && n >= NP) break;
+        const int64_t o = (t * NP + n) * TL + lane;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) out[c * p.vstride + o] = acc[c][r];
+      }
+      continue;
+    }
     const T rx = gg[0 * TL], ry = gg[1 * TL], rz = gg[2 * TL], sx = gg[3 * TL], sy = gg[4 * TL], sz = gg[5 * TL],
             tx = gg[6 * TL], ty = gg[7 * TL], tz = gg[8 * TL];
     T acc[6][R];
@@ -441,46 +509,8 @@ __global__ void __launch_bounds__(TEAMF, 1) fused3d(const dg::StageArgs3 p) {
     }
     const T* gg = sg + lane;
     T acc[6][RF];
-    if constexpr (VSUM) {  // volume by derivative sums: S[d][c] = D_d F_c per row, chain rule per row
-      T S[3][6][RF];
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-#pragma unroll
-        for (int c = 0; c < 6; ++c)
-#pragma unroll
-          for (int r = 0; r < RF; ++r) S[d][c][r] = T(0);
-#pragma unroll 2
-      for (int j = 0; j < NP; ++j) {
-        const T* col = sq + j * TL + lane;
-        T F[6];
-#pragma unroll
-        for (int c = 0; c < 6; ++c) F[c] = col[c * NP * TL];
-#pragma unroll
-        for (int r = 0; r < RF; ++r) {
-          const T4 dd = DV[j * RPD + n0 + r];
-#pragma unroll
-          for (int c = 0; c < 6; ++c) {
-            S[0][c][r] = fma(dd.x, F[c], S[0][c][r]);
-            S[1][c][r] = fma(dd.y, F[c], S[1][c][r]);
-            S[2][c][r] = fma(dd.z, F[c], S[2][c][r]);
-          }
-        }
-      }
-      const T dxv[3] = {gg[0 * TL], gg[3 * TL], gg[6 * TL]}, dyv[3] = {gg[1 * TL], gg[4 * TL], gg[7 * TL]},
-              dzv[3] = {gg[2 * TL], gg[5 * TL], gg[8 * TL]};
-#pragma unroll
-      for (int r = 0; r < RF; ++r) {
-        // d/dx F_c = sum_d dx_d S[d][c] (eq. 6's chain rule, 3D); fields Hx Hy Hz Ex Ey Ez = 0..5
-        auto Dx = [&](int c) { return dxv[0] * S[0][c][r] + dxv[1] * S[1][c][r] + dxv[2] * S[2][c][r]; };
-        auto Dy = [&](int c) { return dyv[0] * S[0][c][r] + dyv[1] * S[1][c][r] + dyv[2] * S[2][c][r]; };
-        auto Dz = [&](int c) { return dzv[0] * S[0][c][r] + dzv[1] * S[1][c][r] + dzv[2] * S[2][c][r]; };
-        acc[0][r] = Dz(4) - Dy(5);  // dHx/dt = -(curl E)_x
-        acc[1][r] = Dx(5) - Dz(3);
-        acc[2][r] = Dy(3) - Dx(4);
-        acc[3][r] = Dy(2) - Dz(1);  // dEx/dt = (curl H)_x
-        acc[4][r] = Dz(0) - Dx(2);
-        acc[5][r] = Dx(1) - Dy(0);
-      }
+    if constexpr (VSUM) {  // volume by derivative sums (volume_sums)
+      volume_sums<RF>(sq, DV, gg, n0, lane, acc);
     } else {  // volume: acc = (-curl E, curl H) of rows n0 .. n0 + R - 1 (volume3d's regrouped chain rule)
       const T rx = gg[0 * TL], ry = gg[1 * TL], rz = gg[2 * TL], sx = gg[3 * TL], sy = gg[4 * TL], sz = gg[5 * TL],
               tx = gg[6 * TL], ty = gg[7 * TL], tz = gg[8 * TL];
