@@ -183,6 +183,9 @@ class ClockSampler:
 
     def __enter__(self):
         self._t.start()
+        t_end = time.perf_counter() + 5.0  # NVML init can take a while: sample before the timed region starts
+        while not self.samples and self._t.is_alive() and time.perf_counter() < t_end:
+            time.sleep(0.005)
         return self
 
     def __exit__(self, *a):

@@ -1,8 +1,9 @@
 #!/bin/bash
 # One GPU pass for the round's evidence (round 2): the GPU test suite and smoke(); bench lines (C4
 # fp32/fp64 fused and split, the tcgen05 variant, C5, C5w, the dry multi-partition run, the reference
-# arm); the ncu launch list of the default bench; full ncu of the stage kernels (5 launches = one
-# LSERK4 step) for C4 fp32, C4 fp64, split C4 fp32, C5 (N=8 fp64 material) and the tcgen05 variant.
+# arm, the 3D order sweep); the ncu launch list of the default bench; full ncu of the stage kernels
+# (5 launches = one LSERK4 step) for C4 fp32, C4 fp64, split C4 fp32, C5 (N=8 fp64 material: the
+# warp-specialised DMMA kernel) and the tcgen05 variant.
 # The ncu captures run first so that the bench lines carry this build's DRAM traffic.
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -q > gpurun_out/gputest.log 2>&1; tail -1 gpurun_out/gputest.log
@@ -38,4 +39,8 @@ python bench.py --config c5 --steps 20 --warmup 3 --ref-n 16 --ref-steps 20 > gp
 python bench.py --config c5w --steps 40 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5w.json 2>> gpurun_out/bench.err
 python bench.py --partitions 4 --steps 100 --warmup 5 > gpurun_out/bench_dry4.json 2>> gpurun_out/bench.err
 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
+rm -f gpurun_out/bench3d.jsonl
+for prec in 4 8; do for n in 1 2 3 4 5; do
+  python bench.py --dim 3 --order $n --prec $prec --steps 20 --warmup 3 --no-cpu-baseline 2>> gpurun_out/bench.err | tail -1 >> gpurun_out/bench3d.jsonl
+done; done
 ls -la gpurun_out
