@@ -83,11 +83,6 @@ constexpr bool DMMA_U = !F32 && DG_MMA == 4;
 #ifndef DG_WS
 #define DG_WS 0
 #endif
-constexpr bool WS = DMMA_U && DG_WS;
-// DG_WS = 2: the helper warps also run the LSERK4 epilogue of the previous tile (the DMMA warps hand the
-// rhs over in a shared-memory buffer and release the tile's fields right after the LIFT: the epilogue
-// reads q_in and the residual from global memory / L2)
-constexpr bool WS2 = WS && DG_WS == 2;
 #ifndef DG_WF
 #define DG_WF 4
 #endif
@@ -105,6 +100,11 @@ constexpr bool USE_TC = F32 && DG_MMA == 3;
 #endif
 constexpr bool TF_SPLIT = USE_TF && DG_MMA == 2;  // 4 warps: m-tile x {Hx, Hy | Ez}
 constexpr bool DMMA_SPLIT = USE_MMA && DG_MMA == 2;  // 2 PR warps: row group x {Hx, Hy | Ez}
+constexpr bool WS = (DMMA_U || (USE_TF && !TF_SPLIT)) && DG_WS;  // fp64 DMMA unit teams; fp32 3xTF32 (2 m-tile warps)
+// DG_WS = 2: the helper warps also run the LSERK4 epilogue of the previous tile (the DMMA warps hand the
+// rhs over in a shared-memory buffer and release the tile's fields right after the LIFT: the epilogue
+// reads q_in and the residual from global memory / L2)
+constexpr bool WS2 = WS && DMMA_U && DG_WS == 2;
 constexpr int PR = (NP + 7) / 8;                     // DMMA row groups (8 output rows each)
 #ifndef DG_R
 #define DG_R (sizeof(DG_T) == 4 ? 8 : 6)
@@ -679,13 +679,20 @@ __device__ __forceinline__ void tmma3(float (&c)[4], const uint32_t (&ah)[4], co
 // (DG_MMA=1: P = 2 warps, one per m-tile), 1 = Hx, Hy (from u, v) and 2 = Ez (from w)
 // (DG_MMA=2: P = 4 warps, m-tile x field set: half the registers per warp, twice the warps).
 // C-fragment register r of n-tile nt is element ee[r >> 1], row 8nt + 2(lane%4) + (r & 1).
-template <int MODE, bool MAT, int FS, typename TT, typename HOOK>
+struct NoHook {
+  __device__ void operator()() const {}
+};
+// WSM (warp-specialised kernel, stage_kernel_ws): the flux is formed by the flux warps -- flux_wait()
+// blocks until this tile's flux is in sp, flux_done() releases sp after the LIFT has read it
+template <int MODE, bool MAT, int FS, bool WSM = false, typename TT, typename HOOK, typename FW = NoHook,
+          typename FD = NoHook>
 __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __restrict__ sq, const TT* __restrict__ sg,
                                         TT* __restrict__ sp, const TT* __restrict__ sr,
                                         const unsigned char* __restrict__ ops, const int32_t (&vmc)[KCODE],
                                         int tile, int g, int mt, int lane, TT alpha, bool read_res,
-                                        const HOOK& after_lift) {
+                                        const HOOK& after_lift, const FW& flux_wait = FW(), const FD& flux_done = FD()) {
   using MT = ModeTraits<MODE>;
+  static_assert(!WSM || (!FLUX_FIRST && !FX && MODE == dg::MODE_FUSED_RK), "warp-specialised tiles: fused stage");
   constexpr int NFLD = FS == 0 ? 3 : (FS == 1 ? 2 : 1);  // output fields F0 .. F0 + NFLD - 1
   constexpr int F0 = FS == 2 ? 2 : 0;
   constexpr bool UV = FS != 2, WW = FS != 1;  // this warp forms u, v (Hx, Hy) / w (Ez)
@@ -830,7 +837,9 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
     }
   }
   if constexpr (MT::surf) {
-    if constexpr (!FLUX_FIRST && !FX) {
+    if constexpr (WSM) {
+      flux_wait();
+    } else if constexpr (!FLUX_FIRST && !FX) {
       flux_points<MAT>(sq, sg + lane, sp, vmc, g, lane, alpha);
       __syncthreads();
     }
@@ -878,6 +887,7 @@ __device__ __forceinline__ void tf_tile(const dg::StageArgs& p, const TT* __rest
       }
     }
   }
+  if constexpr (WSM) flux_done();
   after_lift();  // split pipeline (S = 3): the flux buffer is free, the residual must be in
   if constexpr (MAT) {
     if (MODE != dg::MODE_VOLUME || p.scale_volume) {
@@ -1096,9 +1106,6 @@ __device__ __forceinline__ void mma_tile(const dg::StageArgs& p, const TT* __res
 // Per k-step the warp loads the B fragments of its n-tile once (Ez, and W1, W2 formed from Hx, Hy)
 // and issues them against the A fragments (operator rows) of each of its row groups.  Same algebra as
 // mma_tile: u = Dr Ez, v = Ds Ez, w = Dr W1 + Ds W2 -> flux -> rhs += LIFT f -> 1/mu, 1/eps -> LSERK4.
-struct NoHook {
-  __device__ void operator()() const {}
-};
 // WSM (warp-specialised kernel, stage_kernel_ws): the flux is formed by the flux warps -- flux_wait()
 // blocks until this tile's flux is in sp, flux_done() releases sp after the LIFT has read it
 // WSE (DG_WS = 2): the LSERK4 epilogue runs in the helper warps -- after the LIFT and the material
@@ -1678,8 +1685,11 @@ __host__ __device__ constexpr size_t ws_smem(bool mat) {
   return BARW + OPB_SMEM + 2 * (QB + geo_bytes(mat)) + 2 * SPB + (RES_TMA || WS2 ? QB : 0);
 }
 static_assert(!(WS2 && RES_TMA), "DG_WS = 2 reads the residual in the helper warps (DG_RT = 0)");
+#ifndef DG_WSC
+#define DG_WSC 1  // resident warp-specialised CTAs per SM the register budget is sized for
+#endif
 template <int MODE, bool MAT>
-__global__ void __launch_bounds__(TEAM_WS, 1) stage_kernel_ws(const dg::StageArgs p) {
+__global__ void __launch_bounds__(TEAM_WS, DG_WSC) stage_kernel_ws(const dg::StageArgs p) {
   static_assert(MODE == dg::MODE_FUSED_RK, "the warp-specialised kernel runs the fused stage");
   constexpr int NG = ngeo(MAT);
   constexpr size_t GB = geo_bytes(MAT);
@@ -1737,6 +1747,14 @@ __global__ void __launch_bounds__(TEAM_WS, 1) stage_kernel_ws(const dg::StageArg
     const int4* src = reinterpret_cast<const int4*>(p.ops);
     int4* dst = reinterpret_cast<int4*>(smem_raw + BARW);
     for (int i = tid; i < (int)(OPB_SMEM / 16); i += TEAM_WS) cp_async16(dst + i, src + i);
+    if constexpr (NFE > NF) {  // zero flux pad columns (3xTF32 k-steps of 8) of both flux buffers
+      constexpr int PADN = (NFE - NF) * TL;
+      for (int i = tid; i < 2 * 3 * PADN; i += TEAM_WS) {
+        const int b = i / (3 * PADN), rem = i - b * 3 * PADN;
+        const int c = rem / PADN, rem2 = rem - c * PADN;
+        sp_of(b)[(c * NFE + NF) * TL + rem2] = T(0);
+      }
+    }
   }
   cp_async_commit();
   cp_async_wait_all();
@@ -1785,9 +1803,13 @@ __global__ void __launch_bounds__(TEAM_WS, 1) stage_kernel_ws(const dg::StageArg
         mbar_arrive(bars + 7);  // release: the rhs of tile it is in sacc
         continue;
       }
-      mma_tile_u<MODE, MAT, true>(p, sq_of(b), sg_of(b), sp_of(b), sr, smem_raw + BARW, nocodes, tile, g, lane,
-                                  alpha, read_res, after_lift, flux_wait, flux_done);
-      named_barrier(1, TEAM_M);  // every DMMA warp is done with A[b] and sr
+      if constexpr (USE_TF)
+        tf_tile<MODE, MAT, 0, true>(p, sq_of(b), sg_of(b), sp_of(b), sr, smem_raw + BARW, nocodes, tile, g, g, lane,
+                                    alpha, read_res, after_lift, flux_wait, flux_done);
+      else
+        mma_tile_u<MODE, MAT, true>(p, sq_of(b), sg_of(b), sp_of(b), sr, smem_raw + BARW, nocodes, tile, g, lane,
+                                    alpha, read_res, after_lift, flux_wait, flux_done);
+      named_barrier(1, TEAM_M);  // every contraction warp is done with A[b] and sr
       if (tid == 0) {
         if constexpr (TMA_ST) {  // the new q and residual of the tile, written in place (DG_TS)
           const int64_t t0 = (int64_t)tile * NP * TL;

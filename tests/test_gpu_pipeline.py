@@ -113,10 +113,10 @@ def test_grid_and_tile_order_never_change_the_result(N, prec):
                 assert np.array_equal(a, b), (max_ctas, order)
 
 
-@pytest.mark.parametrize("N", [5, 6, 7, 8])
+@pytest.mark.parametrize("N", [4, 5, 6, 7, 8])
 def test_fp64_dmma_teams_partitions_bitwise(N):
-    """The fp64 DMMA unit teams (N >= 5) and the warp-specialised kernel (DMMA warps + flux warps,
-    N = 6-8): 3 in-process partitions -- the NCCL path's interior-then-boundary tile lists, halo by
+    """The fp64 DMMA unit teams (N >= 4) and the warp-specialised kernel (DMMA warps + flux warps,
+    N = 5-8): 3 in-process partitions -- the NCCL path's interior-then-boundary tile lists, halo by
     device copies -- give bitwise the fields of one partition (P17), as do grid caps and tile order."""
     VX, VY, E, eps, mu, q0, dt, _ = _case(N, False)
     c = dg.dg_setup(N, VX, VY, E, precision=8)
