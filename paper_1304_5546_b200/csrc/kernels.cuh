@@ -198,6 +198,12 @@ constexpr bool RES_TMA = (USE_TF || DMMA_U) && DG_RT;
 #define DG_TS 0
 #endif
 constexpr bool TMA_ST = DG_TS != 0;  // (also the warp-specialised DMMA kernel, stage_kernel_ws)
+// DG_RB (one slot, residual by TMA): the residual arrives on its own mbarrier, waited for after the
+// LIFT, so the top-of-tile wait covers only the fields and geometry the volume phase needs
+#ifndef DG_RB
+#define DG_RB 0
+#endif
+constexpr bool RES_SEP = DG_RB != 0;
 // DG_TS = 2 (3xTF32 path): the same in-place epilogue, but the tile is then written out by all threads
 // with coalesced 16-byte streaming stores (after a barrier) instead of TMA bulk stores
 constexpr bool SMEM_ST = DG_TS == 2;
@@ -1382,7 +1388,8 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       const int s = slot_of_it(it);
       uint64_t* bar = bars + s;
       constexpr bool rt = RES_TMA && MT::rk && !S3;
-      mbar_expect_tx(bar, (unsigned)(QB + GB + (rt && read_res ? QB : 0)));
+      constexpr bool rsep = rt && RES_SEP;  // residual on its own barrier (DG_RB)
+      mbar_expect_tx(bar, (unsigned)(QB + GB + (rt && !rsep && read_res ? QB : 0)));
       T* sq = sq_of(s);
 #pragma unroll
       for (int c = 0; c < 3; ++c)
@@ -1390,9 +1397,11 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
       tma_load_1d(sg_of(s), geo + (int64_t)tile * NG * TL, (unsigned)GB, bar);
       if (rt && read_res) {
         const T* res = static_cast<const T*>(p.res);
+        uint64_t* rbar = rsep ? bars + 2 : bar;
+        if (rsep) mbar_expect_tx(rbar, (unsigned)QB);
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-          tma_load_1d(sr_of(s) + c * NP * TL, res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bar);
+          tma_load_1d(sr_of(s) + c * NP * TL, res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), rbar);
       }
     }
   };
@@ -1442,6 +1451,7 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
   // prologue: barriers, operators (once per persistent CTA), zero flux pad columns, first tiles
   if (tid == 0) {
     for (int b = 0; b < S; ++b) mbar_init(bars + b, 1);  // S = 3: A0, A1, residual
+    if (RES_SEP && S == 1) mbar_init(bars + 2, 1);         // DG_RB: the residual's own barrier
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   {
@@ -1497,6 +1507,9 @@ __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageAr
     // after the LIFT (S = 3): every warp is done with the flux buffer -> the next tile's
     // neighbour gathers go into it; the epilogue then needs this tile's residual
     auto after_lift = [&]() {
+      if constexpr (RES_SEP && S == 1) {
+        if (RES_TMA && MT::rk && read_res) mbar_wait(bars + 2, (unsigned)(it & 1));
+      }
       if constexpr (S3) {
         if constexpr (!GATHER_LATE) {
           __syncthreads();
