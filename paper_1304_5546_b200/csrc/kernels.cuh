@@ -105,6 +105,10 @@ constexpr bool WS = (DMMA_U || (USE_TF && !TF_SPLIT)) && DG_WS;  // fp64 DMMA un
 // rhs over in a shared-memory buffer and release the tile's fields right after the LIFT: the epilogue
 // reads q_in and the residual from global memory / L2)
 constexpr bool WS2 = WS && DMMA_U && DG_WS == 2;
+#ifndef DG_EI
+#define DG_EI 0
+#endif
+constexpr bool EI = WS && DMMA_U && DG_EI;  // the previous tile's epilogue inside the volume k-steps
 constexpr int PR = (NP + 7) / 8;                     // DMMA row groups (8 output rows each)
 #ifndef DG_R
 #define DG_R (sizeof(DG_T) == 4 ? 8 : 6)
@@ -1315,6 +1319,108 @@ __device__ __forceinline__ void mma_tile_u(const dg::StageArgs& p, const TT* __r
   if constexpr (WSM && TMA_ST) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
+
+// DG_EI (warp-specialised DMMA kernel): the LSERK4 epilogue of tile t-1 is interleaved into the
+// volume DMMAs of tile t (epi_step(ks) at every k-step), so its stores and their register hazards
+// overlap the DMMA pipe instead of following the LIFT.  Per tile: volume (+ epilogue steps of the
+// previous tile) -> geometry into registers -> after_volume() (barrier among the DMMA warps: the
+// previous epilogue is done, the tile's residual may be loaded) -> flux_wait() -> release() (the
+// tile's {q, geo} buffer is no longer read: TMA of tile t+2) -> LIFT -> flux_done() -> material
+// scaling -> rhs (held for the next tile's epilogue steps).
+template <bool MAT, typename TT, typename EPI, typename AV_, typename FW, typename REL, typename FD>
+__device__ __forceinline__ void mma_tile_u_ei(const TT* __restrict__ sq, const TT* __restrict__ sg,
+                                              const TT* __restrict__ sp, const unsigned char* __restrict__ ops,
+                                              int g, int lane, TT (&rhs)[UW][3][2], const EPI& epi_step,
+                                              const AV_& after_volume, const FW& flux_wait, const REL& release,
+                                              const FD& flux_done) {
+  using V2 = double2;
+  const int nt = g & 3, rg0 = g >> 2;
+  auto rg_of = [&](int i) { return rg0 + i * UST; };
+  auto unit_ok = [&](int i) { return (UW - 1) * UST + (P / 4 - 1) < PR || rg_of(i) < PR; };
+  const int eb = 8 * nt + (lane >> 2);
+  const int ec0 = 8 * nt + 2 * (lane & 3);
+  const TT rxb = sg[0 * TL + eb], sxb = sg[1 * TL + eb], ryb = sg[2 * TL + eb], syb = sg[3 * TL + eb];
+  TT u[UW][2], v[UW][2], w[UW][2], w2a[UW][2];
+#pragma unroll
+  for (int i = 0; i < UW; ++i) u[i][0] = u[i][1] = v[i][0] = v[i][1] = w[i][0] = w[i][1] = w2a[i][0] = w2a[i][1] = TT(0);
+  const V2* AV = reinterpret_cast<const V2*>(ops);
+  // epilogue steps start EI_LAG k-steps in, so the previous tile's q_in (loaded from L2 at the top of the
+  // tile) has arrived by the time its first step consumes it
+  constexpr int EI_LAG = KV >= 3 * UW + 3 ? 3 : (KV > 3 * UW ? KV - 3 * UW : 0);
+#pragma unroll
+  for (int ks = 0; ks < KV; ++ks) {
+    if (ks >= EI_LAG) epi_step(ks - EI_LAG);
+    const int j = 4 * ks + (lane & 3);
+    const int jc = j < NP ? j : NP - 1;
+    const int addr = jc * TL + colx(jc, eb);
+    const TT ez = sq[2 * NP * TL + addr], hx = sq[addr], hy = sq[NP * TL + addr];
+    const TT w1 = rxb * hy - ryb * hx, w2 = sxb * hy - syb * hx;
+#pragma unroll
+    for (int i = 0; i < UW; ++i) {
+      if (!unit_ok(i)) continue;
+      const V2 a = ldop(AV + (ks * PR + rg_of(i)) * 32 + lane);
+      dmma(u[i][0], u[i][1], a.x, ez);
+      dmma(v[i][0], v[i][1], a.y, ez);
+      dmma(w[i][0], w[i][1], a.x, w1);
+      dmma(w2a[i][0], w2a[i][1], a.y, w2);
+    }
+  }
+#pragma unroll
+  for (int ks = KV - EI_LAG; ks < 3 * UW; ++ks) epi_step(ks);  // (k-steps fewer than epilogue steps)
+  TT gx[2][4], mf[2][2];  // the tile's geometry (and material factors) of this lane's two elements
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int ec = ec0 + h;
+    gx[h][0] = sg[0 * TL + ec];
+    gx[h][1] = sg[1 * TL + ec];
+    gx[h][2] = sg[2 * TL + ec];
+    gx[h][3] = sg[3 * TL + ec];
+    if constexpr (MAT) {
+      mf[h][0] = sg[16 * TL + ec];
+      mf[h][1] = sg[17 * TL + ec];
+    }
+  }
+  after_volume();
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < UW; ++i) {
+      const TT rx = gx[h][0], sx = gx[h][1], ry = gx[h][2], sy = gx[h][3];
+      rhs[i][2][h] = w[i][h] + w2a[i][h];
+      rhs[i][0][h] = -(ry * u[i][h] + sy * v[i][h]);
+      rhs[i][1][h] = rx * u[i][h] + sx * v[i][h];
+    }
+  flux_wait();
+  release();
+  const TT* AL = reinterpret_cast<const TT*>(ops + DVB);
+#pragma unroll
+  for (int ks = 0; ks < KL; ++ks) {
+    const int m = 4 * ks + (lane & 3);
+    const int mc = m < NF ? m : NF - 1;
+    const int addr = mc * TL + colx(mc, eb);
+    const TT f0 = sp[0 * NFE * TL + addr], f1 = sp[1 * NFE * TL + addr], f2 = sp[2 * NFE * TL + addr];
+#pragma unroll
+    for (int i = 0; i < UW; ++i) {
+      if (!unit_ok(i)) continue;
+      const TT a = ldop(AL + (ks * PR + rg_of(i)) * 32 + lane);
+      dmma(rhs[i][0][0], rhs[i][0][1], a, f0);
+      dmma(rhs[i][1][0], rhs[i][1][1], a, f1);
+      dmma(rhs[i][2][0], rhs[i][2][1], a, f2);
+    }
+  }
+  flux_done();
+  if constexpr (MAT) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int i = 0; i < UW; ++i) {
+        rhs[i][0][h] *= mf[h][0];
+        rhs[i][1][h] *= mf[h][0];
+        rhs[i][2][h] *= mf[h][1];
+      }
+  }
+}
+
 // Persistent, software-pipelined stage kernel (one team per CTA).
 template <int MODE, bool MAT>
 __global__ void __launch_bounds__(TEAM, MIN_CTAS) stage_kernel(const dg::StageArgs p) {
@@ -1778,7 +1884,82 @@ __global__ void __launch_bounds__(TEAM_WS, DG_WSC) stage_kernel_ws(const dg::Sta
     if (n_it > 2) prefetch_l2(2);
   }
   const T alpha = static_cast<T>(p.alpha);
-  if (g < P) {  // ------------------------------------------------------------- DMMA warps
+  if (EI && g < P) {  // ---------------------------------- DMMA warps, interleaved epilogue (DG_EI)
+    static_assert(!EI || (RES_TMA && !TMA_ST && !WS2), "DG_EI: residual by TMA, streaming stores");
+    using V2 = double2;
+    const int nt = g & 3, rg0 = g >> 2;
+    const int ec0 = 8 * nt + 2 * (lane & 3);
+    const T a = static_cast<T>(p.a), bq = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
+    T pend[UW][3][2];  // rhs of the previous tile, applied by the epilogue steps
+    int ptile = -1;    // the previous tile (-1: none)
+    auto unit_n = [&](int i) { return 8 * (rg0 + i * UST) + (lane >> 2); };
+    V2 qpre[UW][3];    // q_in of the previous tile (global / L2), loaded before the first epilogue step
+    auto epi_step = [&](int k) {
+      if (ptile < 0 || k >= 3 * UW) return;
+      const int i = k / 3, c = k % 3;
+      const int n = unit_n(i);
+      if (n >= NP) return;
+      const int col = colx(n, ec0);
+      const int64_t off = ((int64_t)ptile * NP + n) * TL + col;
+      V2 rs;
+      rs.x = dt * pend[i][c][0];
+      rs.y = dt * pend[i][c][1];
+      if (read_res) {
+        const V2 ro = *reinterpret_cast<const V2*>(sr + (c * NP + n) * TL + col);
+        rs.x = fma(a, ro.x, rs.x);
+        rs.y = fma(a, ro.y, rs.y);
+      }
+      V2 qn;
+      qn.x = fma(bq, rs.x, qpre[i][c].x);
+      qn.y = fma(bq, rs.y, qpre[i][c].y);
+      if (p.write_res) st_out(reinterpret_cast<V2*>(static_cast<T*>(p.res) + c * p.vstride + off), rs);
+      st_out(reinterpret_cast<V2*>(static_cast<T*>(p.q_out) + c * p.fstride + off), qn);
+    };
+    auto load_qpre = [&]() {
+      if (ptile < 0) return;
+#pragma unroll
+      for (int i = 0; i < UW; ++i) {
+        const int n = unit_n(i);
+        const int nc = n < NP ? n : NP - 1;
+        const int64_t off = ((int64_t)ptile * NP + nc) * TL + colx(nc, ec0);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) qpre[i][c] = __ldg(reinterpret_cast<const V2*>(q + c * p.fstride + off));
+      }
+    };
+    for (int it = 0; it < n_it; ++it) {
+      const int b = it & 1;
+      const int tile = tile_of(it);
+      load_qpre();
+      if (ptile >= 0 && read_res) mbar_wait(bars + 2, (unsigned)((it - 1) & 1));  // residual of tile it-1
+      mbar_wait(bars + b, (unsigned)((it >> 1) & 1));
+      auto after_volume = [&]() {
+        named_barrier(1, TEAM_M);  // every DMMA warp is done with the previous epilogue (sr) and the volume
+        if (read_res && tid == 0) {
+          mbar_expect_tx(bars + 2, (unsigned)QB);
+          const T* res = static_cast<const T*>(p.res);
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            tma_load_1d(sr + c * NP * TL, res + c * p.vstride + (int64_t)tile * NP * TL, (unsigned)(QB / 3), bars + 2);
+        }
+      };
+      auto flux_wait = [&]() { mbar_wait(bars + 3 + b, (unsigned)((it >> 1) & 1)); };
+      auto release = [&]() {  // the flux warps are done with A[b] (flux of tile it), the DMMA warps too
+        if (tid == 0) {
+          if (it + 2 < n_it) issue_tma(it + 2);
+          if (it + 3 < n_it) prefetch_l2(it + 3);
+        }
+      };
+      auto flux_done = [&]() { mbar_arrive(bars + 5 + b); };
+      mma_tile_u_ei<MAT>(sq_of(b), sg_of(b), sp_of(b), smem_raw + BARW, g, lane, pend, epi_step, after_volume,
+                         flux_wait, release, flux_done);
+      ptile = tile;
+    }
+    // the last tile's epilogue
+    load_qpre();
+    if (read_res) mbar_wait(bars + 2, (unsigned)((n_it - 1) & 1));
+#pragma unroll
+    for (int k = 0; k < 3 * UW; ++k) epi_step(k);
+  } else if (g < P) {  // ------------------------------------------------------------- DMMA warps
     const int32_t nocodes[KCODE] = {};
     for (int it = 0; it < n_it; ++it) {
       const int b = it & 1;
