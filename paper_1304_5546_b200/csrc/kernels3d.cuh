@@ -448,7 +448,10 @@ __global__ void __launch_bounds__(TEAMS, 1) surface3d(const dg::StageArgs3 p) {
 // registers (warp g: rows [gR, gR + R)); the flux of this warp's face points m = g + kP reads own and
 // same-tile neighbour traces from shared memory, other neighbours from global memory / L2; the
 // LSERK4 residual of the warp's rows is loaded at the top of the tile.  No rhsV round trip.
-__global__ void __launch_bounds__(TEAMF, 1) fused3d(const dg::StageArgs3 p) {
+#ifndef DG_F3C
+#define DG_F3C 1  // resident fused CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(TEAMF, DG_F3C) fused3d(const dg::StageArgs3 p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
   const T4* DV = reinterpret_cast<const T4*>(smem_raw + BARB);

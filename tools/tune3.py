@@ -26,7 +26,9 @@ GRID3 = [dict(SQ=sq, RS=1, R=r) for sq, r in itertools.product((0, 1), (4, 16))]
 GRIDF = [dict(RF=r) for r in (1, 2, 4, 8)]
 # the fused kernel's volume by derivative sums (VS = 1) against the W form (VS = 0)
 GRIDV = [dict(VS=v, RF=r) for v in (0, 1) for r in (1, 2, 4)]
-GRID = {"2": GRID2, "3": GRID3, "fused": GRIDF, "vs": GRIDV}.get(os.environ.get("TUNE3_GRID", ""), GRID)
+# resident fused CTAs per SM the registers are sized for (F3C), on top of each module's tuned RF / VS
+GRIDC = [dict(F3C=c) for c in (2, 3, 4)]
+GRID = {"2": GRID2, "3": GRID3, "fused": GRIDF, "vs": GRIDV, "f3c": GRIDC}.get(os.environ.get("TUNE3_GRID", ""), GRID)
 
 
 def name(k):
@@ -37,7 +39,7 @@ def build():
     from paper_1304_5546_b200 import build as B
 
     for k in GRID:
-        print(B.build_variant3(name(k), k, VDIR), flush=True)
+        print(B.build_variant3(name(k), k, VDIR, merge=os.environ.get("TUNE3_GRID") == "f3c"), flush=True)
 
 
 def run(out="gpurun_out/tune3.jsonl", steps=20):
