@@ -1,3 +1,6 @@
+# Same-box A/B of the 3D order sweep: the in-tree library against a variant library (here the
+# PF=0 build of the surface-prefetch experiment, packed as build_modvar/v3/pf0.so by hand; see
+# profiles/r02_bench3d_pf_ab.txt).  Run on the GPU box from the repo root.
 tar xzf build_modvar.tgz
 for lib in main build_modvar/v3/pf0.so; do
  for prec in 4 8; do for n in 1 2 3 4 5; do
