@@ -72,6 +72,17 @@ constexpr bool VSUM = DG_VS;
                   // the one tuned case that runs it, its 18 R sums spill
 #endif
 constexpr bool VSUMV = DG_VSV;
+// DG_G3 (fused kernel), the neighbour traces of the flux:
+//   0  codes and traces loaded inside the flux loop (code -> trace: two dependent L2 round trips)
+//   1  codes loaded at the top of the tile into registers, the cross-tile traces gathered by cp.async
+//      into the flux buffer there too (each thread its own face points); measured slower
+//   2  codes loaded at the top of the tile into registers (their latency hides behind the volume),
+//      traces from L2 in the (fully unrolled) flux loop
+#ifndef DG_G3
+#define DG_G3 0
+#endif
+constexpr bool G3 = DG_G3 == 1;
+constexpr bool PRECODE = DG_G3 != 0;
 constexpr int RPD = RP > RPF ? RP : RPF;  // operator-row padding of DV (volume and fused kernels)
 // operator block: DV[j][n] = {Dr, Ds, Dt, 0} [NP][RP], LV[m][n] [NF][RP], fmask [NF] int32
 struct alignas(4 * sizeof(T)) T4 { T x, y, z, w; };
@@ -125,6 +136,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -501,6 +518,27 @@ __global__ void __launch_bounds__(TEAMF, DG_F3C) fused3d(const dg::StageArgs3 p)
       for (int c = 0; c < 6; ++c) prefetch_l2(q + c * p.fstride + t1 * NP * TL, (unsigned)(NP * TL * sizeof(T)));
       prefetch_l2(geo + t1 * NG * TL, (unsigned)GB);
     }
+    const int32_t* codes = p.vmapP + t * NF * TL + lane;
+    int32_t cc[(NF + PF - 1) / PF];  // neighbour codes of this thread's face points m = g + k PF (PRECODE)
+    if constexpr (PRECODE) {
+#pragma unroll
+      for (int k = 0; k < (NF + PF - 1) / PF; ++k) {
+        const int m = g + k * PF;
+        cc[k] = m < NF ? __ldg(codes + m * TL) : -1;
+      }
+    }
+    if constexpr (G3) {  // cross-tile neighbour traces -> sp (the previous tile's LIFT is done with it)
+#pragma unroll
+      for (int k = 0; k < (NF + PF - 1) / PF; ++k) {
+        const int m = g + k * PF;
+        if (m < NF && cc[k] >= 0) {
+#pragma unroll
+          for (int c = 0; c < 6; ++c)
+            cp_async_small<sizeof(T)>(sp + (c * NF + m) * TL + lane, q + cc[k] + c * p.fstride);
+        }
+      }
+      cp_async_commit();
+    }
     // the LSERK4 residual of this warp's rows (in flight during the volume and surface phases)
     T rr[6][RF];
 #pragma unroll
@@ -546,16 +584,18 @@ __global__ void __launch_bounds__(TEAMF, DG_F3C) fused3d(const dg::StageArgs3 p)
       }
     }
     // flux of this warp's face points into sp (surface3d's upwind flux, 1/2 of the jump form)
-    const int32_t* codes = p.vmapP + t * NF * TL + lane;
-#pragma unroll 4
+    if constexpr (G3) cp_async_wait_all();  // this thread's own gathers
+#pragma unroll (PRECODE ? KPF : 4)
     for (int k = 0; k < KPF; ++k) {
       const int m = g + k * PF;
       if (m >= NF) break;
       const int f = m / NFP;
       const int fm = fmask[m];
-      const int32_t code = __ldg(codes + m * TL);
-      const T* pn = code >= 0 ? q + code : sq + (-1 - code);
-      const int64_t fsn = code >= 0 ? p.fstride : (int64_t)NP * TL;
+      int32_t code;
+      if constexpr (PRECODE) code = cc[k];
+      else code = __ldg(codes + m * TL);
+      const T* pn = code >= 0 ? (G3 ? sp + m * TL + lane : q + code) : sq + (-1 - code);
+      const int64_t fsn = code >= 0 ? (G3 ? (int64_t)NF * TL : p.fstride) : (int64_t)NP * TL;
       T own[6], nb[6];
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
