@@ -111,7 +111,13 @@ constexpr bool PF3 = DG_PF3;
 constexpr size_t SMEM_SURF = STAGEQ ? SMEM_SURF_Q : LVB + FMB + SPB;
 static_assert(SMEM_VOL <= 227 * 1024 && SMEM_SURF <= 227 * 1024, "3D kernel shared memory");
 // fused stage kernel (volume + flux + LIFT + LSERK4, one launch per stage) when its tile fits
-constexpr size_t SMEM_FUSED = BARB + DVB + LVB + FMB + QB + GB + SPB;
+// DG_D3: the fused kernel double-buffers the tile's {fields, geometry} (the next tile's TMA is issued at
+// the top of the current one) where the second buffer fits
+#ifndef DG_D3
+#define DG_D3 0
+#endif
+constexpr bool D3 = DG_D3 && BARB + DVB + LVB + FMB + 2 * (QB + GB) + SPB <= 227 * 1024;
+constexpr size_t SMEM_FUSED = BARB + DVB + LVB + FMB + (D3 ? 2 : 1) * (QB + GB) + SPB;
 #ifndef DG_F3
 #define DG_F3 1
 #endif
@@ -474,9 +480,11 @@ __global__ void __launch_bounds__(TEAMF, DG_F3C) fused3d(const dg::StageArgs3 p)
   const T4* DV = reinterpret_cast<const T4*>(smem_raw + BARB);
   const T* LV = reinterpret_cast<const T*>(smem_raw + BARB + DVB);
   const int32_t* fmask = reinterpret_cast<const int32_t*>(smem_raw + BARB + DVB + LVB);
-  T* sq = reinterpret_cast<T*>(smem_raw + BARB + DVB + LVB + FMB);
-  T* sg = reinterpret_cast<T*>(smem_raw + BARB + DVB + LVB + FMB + QB);
+  T* const sq0 = reinterpret_cast<T*>(smem_raw + BARB + DVB + LVB + FMB);
+  T* const sg0 = reinterpret_cast<T*>(smem_raw + BARB + DVB + LVB + FMB + QB);
   T* sp = reinterpret_cast<T*>(smem_raw + BARB + DVB + LVB + FMB + QB + GB);
+  T* const sq1 = D3 ? reinterpret_cast<T*>(smem_raw + BARB + DVB + LVB + FMB + QB + GB + SPB) : sq0;  // DG_D3
+  T* const sg1 = D3 ? sq1 + (size_t)6 * NP * TL : sg0;
   const T* __restrict__ q = static_cast<const T*>(p.q_in);
   const T* __restrict__ geo = static_cast<const T*>(p.geo);
   const int tid = threadIdx.x, g = tid >> 5, lane = tid & 31, n0 = g * RF;
@@ -487,15 +495,19 @@ __global__ void __launch_bounds__(TEAMF, DG_F3C) fused3d(const dg::StageArgs3 p)
   auto issue = [&](int it) {
     if (tid == 0) {
       const int64_t t = first + (int64_t)it * stride;
-      mbar_expect_tx(bar, (unsigned)(QB + GB));
+      uint64_t* bb = bar + (D3 ? (it & 1) : 0);
+      T* dq = D3 && (it & 1) ? sq1 : sq0;
+      T* dg = D3 && (it & 1) ? sg1 : sg0;
+      mbar_expect_tx(bb, (unsigned)(QB + GB));
 #pragma unroll
       for (int c = 0; c < 6; ++c)
-        tma_load_1d(sq + c * NP * TL, q + c * p.fstride + t * NP * TL, (unsigned)(NP * TL * sizeof(T)), bar);
-      tma_load_1d(sg, geo + t * NG * TL, (unsigned)GB, bar);
+        tma_load_1d(dq + c * NP * TL, q + c * p.fstride + t * NP * TL, (unsigned)(NP * TL * sizeof(T)), bb);
+      tma_load_1d(dg, geo + t * NG * TL, (unsigned)GB, bb);
     }
   };
   if (tid == 0) {
     mbar_init(bar, 1);
+    if (D3) mbar_init(bar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   {
@@ -510,8 +522,11 @@ __global__ void __launch_bounds__(TEAMF, DG_F3C) fused3d(const dg::StageArgs3 p)
   const T a = static_cast<T>(p.a), b = static_cast<T>(p.b), dt = static_cast<T>(p.dt);
   for (int it = 0; it < n_it; ++it) {
     const int64_t t = first + (int64_t)it * stride;
-    mbar_wait(bar, (unsigned)(it & 1));
+    T* const sq = D3 && (it & 1) ? sq1 : sq0;
+    T* const sg = D3 && (it & 1) ? sg1 : sg0;
+    mbar_wait(bar + (D3 ? (it & 1) : 0), (unsigned)(D3 ? ((it >> 1) & 1) : (it & 1)));
     __syncthreads();
+    if (D3 && it + 1 < n_it) issue(it + 1);  // the other buffer: tile it-1 is done with it
     if (it + 1 < n_it && tid == 0) {
       const int64_t t1 = t + stride;
 #pragma unroll
@@ -646,7 +661,7 @@ __global__ void __launch_bounds__(TEAMF, DG_F3C) fused3d(const dg::StageArgs3 p)
         __stcs(qo + c * p.fstride + o, fma(b, rs, sq[(c * NP + n) * TL + lane]));
       }
     }
-    if (it + 1 < n_it) {
+    if (!D3 && it + 1 < n_it) {
       __syncthreads();  // every thread is done with the tile's fields and flux
       issue(it + 1);
     }
