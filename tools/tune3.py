@@ -29,8 +29,9 @@ GRIDV = [dict(VS=v, RF=r) for v in (0, 1) for r in (1, 2, 4)]
 # resident fused CTAs per SM the registers are sized for (F3C), on top of each module's tuned RF / VS
 GRIDC = [dict(F3C=c) for c in (2, 3, 4)]
 GRIDD = [dict(D3=1)]  # double-buffered fused tiles (A/B against main)
+GRIDR = [dict(RF=r, G3=g) for r in (1, 2, 4) for g in (0, 2)]  # RF re-tune with the code preload
 GRIDG = [dict(G3=2), dict(G3=1)]  # neighbour codes preloaded (2), + cp.async gathers (1), A/B against main (0)
-GRID = {"2": GRID2, "3": GRID3, "fused": GRIDF, "vs": GRIDV, "f3c": GRIDC, "g3": GRIDG, "d3": GRIDD}.get(os.environ.get("TUNE3_GRID", ""), GRID)
+GRID = {"2": GRID2, "3": GRID3, "fused": GRIDF, "vs": GRIDV, "f3c": GRIDC, "g3": GRIDG, "d3": GRIDD, "rfg": GRIDR}.get(os.environ.get("TUNE3_GRID", ""), GRID)
 
 
 def name(k):
@@ -41,7 +42,7 @@ def build():
     from paper_1304_5546_b200 import build as B
 
     for k in GRID:
-        print(B.build_variant3(name(k), k, VDIR, merge=os.environ.get("TUNE3_GRID") in ("f3c", "g3", "d3")), flush=True)
+        print(B.build_variant3(name(k), k, VDIR, merge=os.environ.get("TUNE3_GRID") in ("f3c", "g3", "d3", "rfg")), flush=True)
 
 
 def run(out="gpurun_out/tune3.jsonl", steps=20):
