@@ -182,11 +182,12 @@ def test_partitioned_group_bitwise_equals_single(P, fused, order):
 
 
 
-@pytest.mark.parametrize("N,prec", [(5, 4), (5, 8), (8, 8), (7, 4), (1, 4)])
+@pytest.mark.parametrize("N,prec", [(5, 4), (5, 8), (8, 8), (7, 4), (1, 4), (4, 8), (6, 8)])
 @pytest.mark.parametrize("n", [1, 4])
 def test_tiny_meshes_single_partial_tile(N, prec, n):
     """Edge cases: n=1 (K=2, one tile of which 30 columns are padding) and n=4 (K=32, exactly
-    one full tile, no ragged tail), on every contraction path (FMA, 3xTF32, DMMA, 3xTF32 split)."""
+    one full tile, no ragged tail), on every contraction path (FMA, 3xTF32, DMMA unit teams, the
+    warp-specialised fp64 kernel at N = 5, 6, 8, 3xTF32 split)."""
     VX, VY, E = dginputs.rect_mesh(n)
     o = Oracle(N, VX, VY, E)
     q0 = _initial(o, amp=1e-2)
