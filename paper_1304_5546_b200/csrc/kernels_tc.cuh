@@ -26,6 +26,15 @@
 
 namespace tc {
 
+// DG_TCP: the neighbour codes of group it+1 are loaded into registers while group it computes, so
+// the traces' loads at the top of a group do not first wait for their codes
+#ifndef DG_TCP
+#define DG_TCP 1
+#endif
+// DG_TCR: the L2 prefetch of a group (one ahead) also covers its LSERK4 residual (measured 6% slower: off)
+#ifndef DG_TCR
+#define DG_TCR 0
+#endif
 constexpr int TG = 4;                    // tiles per group
 constexpr int MG = TG * TL;              // MMA M = 128 elements
 // DG_TH threads per element (1 or 2): thread (element e, half h) owns columns 8k + CW h .. + CW - 1 of
@@ -217,6 +226,11 @@ __global__ void __maxnreg__(TC_MAXREG) stage_kernel_tc(const dg::StageArgs p) {
       for (int c = 0; c < 3; ++c) bulk_prefetch_l2(q + c * p.fstride + g * FS, (unsigned)QF);
       bulk_prefetch_l2(geo + g * TG * NG * TL, (unsigned)GB);
       if (MT::surf) bulk_prefetch_l2(p.vmapP + g * TG * NF * TL, (unsigned)(TG * NF * TL * 4));
+      if (DG_TCR && MT::rk && p.a != 0.0) {  // the LSERK4 residual the epilogue reads (DG_TCR)
+        const float* res = static_cast<const float*>(p.res);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) bulk_prefetch_l2(res + c * p.vstride + g * FS, (unsigned)QF);
+      }
     }
   };
 
@@ -256,6 +270,13 @@ __global__ void __maxnreg__(TC_MAXREG) stage_kernel_tc(const dg::StageArgs p) {
   auto mark = [](int) {};
 #endif
 
+  int32_t vcn[KC];
+  auto load_codes = [&](int it2, int32_t (&v)[KC]) {
+    const int32_t* src = p.vmapP + (group_of(it2) * TG + ti) * NF * TL + lane;
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) v[kk] = point(kk) < NF ? __ldg(src + point(kk) * TL) : -1;
+  };
+  if (DG_TCP && MT::surf) load_codes(0, vcn);
   for (int it = 0; it < n_it; ++it) {
     const int64_t grp = group_of(it);
     // neighbour codes of this thread's face points (L2: prefetched one group ahead), then the
@@ -263,13 +284,17 @@ __global__ void __maxnreg__(TC_MAXREG) stage_kernel_tc(const dg::StageArgs p) {
     int32_t vc[KC];
     float nb[3][KC];
     if constexpr (MT::surf) {
-      const int32_t* src = p.vmapP + (grp * TG + ti) * NF * TL + lane;
+      if constexpr (DG_TCP) {
 #pragma unroll
-      for (int kk = 0; kk < KC; ++kk) vc[kk] = point(kk) < NF ? __ldg(src + point(kk) * TL) : -1;
+        for (int kk = 0; kk < KC; ++kk) vc[kk] = vcn[kk];
+      } else {
+        load_codes(it, vc);
+      }
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk)
 #pragma unroll
         for (int c = 0; c < 3; ++c) nb[c][kk] = vc[kk] >= 0 ? __ldg(q + vc[kk] + c * p.fstride) : 0.f;
+      if (DG_TCP && it + 1 < n_it) load_codes(it + 1, vcn);
     }
     mbar_wait(bar_tma + (it % NB), (unsigned)((it / NB) & 1));
     mark(0);
