@@ -35,6 +35,11 @@ namespace tc {
 #ifndef DG_TCR
 #define DG_TCR 0
 #endif
+// DG_TCE: the LSERK4 residual of the whole group loaded at its top (see the group loop)
+#ifndef DG_TCE
+#define DG_TCE 0
+#endif
+constexpr bool TCE = DG_TCE;
 constexpr int TG = 4;                    // tiles per group
 constexpr int MG = TG * TL;              // MMA M = 128 elements
 // DG_TH threads per element (1 or 2): thread (element e, half h) owns columns 8k + CW h .. + CW - 1 of
@@ -303,6 +308,24 @@ __global__ void __maxnreg__(TC_MAXREG) stage_kernel_tc(const dg::StageArgs p) {
     if (NB == 2 && it + 1 < n_it) issue_tma(it + 1);
     if (NB == 1 && it + 1 < n_it) prefetch_l2(it + 1);  // its TMA is issued after this group
     if (NB == 2 && it + 2 < n_it) prefetch_l2(it + 2);
+    // DG_TCE: the whole LSERK4 residual of this thread's nodes is loaded here, in flight during the
+    // volume and flux phases, instead of one 8-node chunk ahead inside the epilogue
+    float rall[TCE ? KSV : 1][3][CW];
+    if constexpr (TCE && MT::rk) {
+      if (read_res) {
+        const int64_t tb0 = ((grp * TG + ti) * NP) * TL + lane;
+        const float* __restrict__ res0 = static_cast<const float*>(p.res);
+#pragma unroll
+        for (int ks = 0; ks < KSV; ++ks)
+#pragma unroll
+          for (int j = 0; j < CW; ++j) {
+            const int n = 8 * ks + CW * h + j;
+            const int64_t o = tb0 + (n < NP ? n : NP - 1) * TL;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) rall[ks][c][j] = __ldcs(res0 + c * p.vstride + o);
+          }
+      }
+    }
     const float* sq = sq_of(it);
     const float* gg = sg_of(it) + ti * NG * TL + lane;  // this element's geometry column
     const float rx = gg[0 * TL], sx = gg[1 * TL], ry = gg[2 * TL], sy = gg[3 * TL];
@@ -439,7 +462,7 @@ __global__ void __maxnreg__(TC_MAXREG) stage_kernel_tc(const dg::StageArgs p) {
       }
     };
     float ra[3][CW], rb[3][CW];
-    load_res(0, ra);
+    if constexpr (!TCE) load_res(0, ra);
     mark(9);
     mbar_wait(bar_mma, mma_par);
     mma_par ^= 1u;
@@ -448,8 +471,8 @@ __global__ void __maxnreg__(TC_MAXREG) stage_kernel_tc(const dg::StageArgs p) {
     const float a = static_cast<float>(p.a), b = static_cast<float>(p.b), dt = static_cast<float>(p.dt);
 #pragma unroll
     for (int ks = 0; ks < KSV; ++ks) {
-      float (&rv)[3][CW] = (ks & 1) ? rb : ra;
-      if (ks + 1 < KSV) {
+      float (&rv)[3][CW] = TCE ? rall[TCE ? ks : 0] : ((ks & 1) ? rb : ra);
+      if (!TCE && ks + 1 < KSV) {
         if (ks & 1) load_res(ks + 1, ra);
         else load_res(ks + 1, rb);
       }
