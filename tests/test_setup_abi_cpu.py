@@ -42,7 +42,7 @@ def test_kernel_config_matches_tune_table(prec):
         k = c.kernel_config()
         c.destroy()
         t = tune[f"N{N}_{'f32' if prec == 4 else 'f64'}"]
-        want = ("3xtf32" if prec == 4 else "dmma_fp64") if t["M"] else "fma"
+        want = ("tcgen05_3xtf32" if t["M"] == 3 else "3xtf32" if prec == 4 else "dmma_fp64") if t["M"] else "fma"
         assert k["contraction"] == want, (N, k)
         assert k["slots"] == t["S"] and k["teams_cap"] == t["C"]
         # residual staged by TMA: the 3xTF32 path (fp32) and the DMMA unit teams (fp64, M=4), knob Q
