@@ -21,8 +21,10 @@ def build(tag, specs):
     from paper_1304_5546_b200 import build as B
     B.build()
     n = int(tag[1:tag.index("_")])
-    ct = "float" if tag.endswith("f32") else "double"
+    ct = "float" if "_f32" in tag else "double"
     base = dict(B.tuning().get(tag, {}))
+    if tag.endswith("_tc"):  # the tcgen05 variant module
+        base = dict(B.TC_DEFAULT, **base, M=3, V=1)
     base.pop("ms", None)
     vdir = os.path.join(OUT, tag)
     os.makedirs(vdir, exist_ok=True)
@@ -72,7 +74,7 @@ if @MAT@:  # two-layer material (C5's recipe, dginputs.two_layer_material)
     eps, mu = dginputs.two_layer_material(VX, VY, E)
     kw = dict(eps=eps, mu=mu)
     dt = dginputs.cfl_dt(VX, VY, E, N, eps=eps, mu=mu)
-c = dg.dg_setup(N, VX, VY, E, precision=PREC, **kw)
+c = dg.dg_setup(N, VX, VY, E, precision=PREC, kernel_variant=@KV@, **kw)
 x, y = c.nodes()
 c.set_fields(*dginputs.cavity_mode(x, y, dginputs.C4_T0))
 c.run(dt, 3); c.sync()
@@ -84,7 +86,7 @@ for rep in range(3):
     ms.append(e0.elapsed_time(e1) / (5 * @STEPS@))
 cfg = c.kernel_config(); c.destroy()
 G = np.load(@ROOT@ + "/tests/golden/pipeline_gate_n12.npz")
-g = dg.dg_setup(N, G["VX"], G["VY"], G["EToV"], precision=PREC, max_ctas=2)
+g = dg.dg_setup(N, G["VX"], G["VY"], G["EToV"], precision=PREC, max_ctas=2, kernel_variant=@KV@)
 xg, yg = g.nodes()
 q0 = dginputs.cavity_mode(xg, yg, float(G["t0_%d" % N]))
 q0 = tuple(a + b for a, b in zip(q0, dginputs.perturbation(xg.shape, float(G["amplitude"]), seed=N)))
@@ -96,12 +98,12 @@ print(json.dumps(dict(N=N, prec=PREC, n=@NN@, mat=bool(@MAT@), ms=min(ms), ms_al
 
 def time_all(tag, out, n=362, mat=False, steps=20):
     N = int(tag[1:tag.index("_")])
-    prec = 4 if tag.endswith("f32") else 8
+    prec = 4 if "_f32" in tag else 8
     vdir = os.path.join(OUT, tag)
     libs = [("main", None)] + [(f[:-3], os.path.join(vdir, f)) for f in sorted(os.listdir(vdir)) if f.endswith(".so")]
     code = CODE
     for k, v in (("@ROOT@", repr(ROOT)), ("@NN@", str(n)), ("@N@", str(N)), ("@PREC@", str(prec)),
-                 ("@MAT@", str(int(mat))), ("@STEPS@", str(steps))):
+                 ("@MAT@", str(int(mat))), ("@STEPS@", str(steps)), ("@KV@", "1" if tag.endswith("_tc") else "0")):
         code = code.replace(k, v)
     os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
     with open(out, "a") as fh:
